@@ -1,0 +1,339 @@
+/*
+ * abin_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct CPU oracle for the hot path of
+ * Chan, "Memory-efficient and fast implementation of local adaptive
+ * binarization methods" (arXiv 1905.13038), reference/PAPER.md.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library. The product path
+ * (paper_1905_13038_b200/) never links, imports or executes it, and this
+ * file shares no code, header, table or constant generator with the CUDA
+ * path.
+ *
+ * Everything here is the *definition* written out (Sec. 1,
+ * l.27: m and s as direct sums over the h x w window) -- Theta(HWhw) --
+ * with the paper's window offsets (Alg. 1 l.1-4), the
+ * "undefined elements are zero" border convention and the
+ * clamped count n (Alg. 1).  Thresholds follow Table 1
+ * evaluated left to right in IEEE double, compiled
+ * with -ffp-contract=off -fno-fast-math.
+ *
+ * Secondary engines (each exact, each pinned against orc_* direct in the
+ * CPU tests):
+ *   orc_alg1_stats   -- a literal transcription of Algorithm 1's recursion
+ *                       (PAPER.md:98-120), used as the "decomposition
+ *                       invariance" pin and as the paper-method CPU timing.
+ *   orc_integral_stats -- Sec. 2 integral images, u64.
+ *
+ * Parity unpinned (no value in the paper fixes them):
+ *   - the exact fp64 bits of t (pinned only by the literal Table-1 order);
+ *   - the quantile rank convention rho = max(1, ceil(q n)) (SPEC choice).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORC_SAUVOLA 0
+#define ORC_NIBLACK 1
+#define ORC_WOLF 2
+
+/* Alg. 1 l.1-4. */
+static void offsets(int32_t h, int32_t w, int64_t *l, int64_t *r, int64_t *o, int64_t *u) {
+  *l = (w + 1) / 2; /* floor((w+1)/2) */
+  *r = w / 2;       /* floor(w/2)     */
+  *o = (h + 1) / 2; /* floor((h+1)/2) */
+  *u = h / 2;       /* floor(h/2)     */
+}
+
+static int64_t mn(int64_t a, int64_t b) { return a < b ? a : b; }
+static int64_t mx(int64_t a, int64_t b) { return a > b ? a : b; }
+
+int orc_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+void orc_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
+/* Window offsets exported for the tests (they are pinned against the SPEC
+ * examples and against brute-force enumeration of PAPER.md:27's bounds). */
+void orc_offsets(int32_t h, int32_t w, int64_t out4[4]) {
+  offsets(h, w, &out4[0], &out4[1], &out4[2], &out4[3]);
+}
+
+/* n, PAPER.md:118:
+ *   n = (min{j+r, W-1} - max{j-l, -1}) * (min{i+u, H-1} - max{i-o, -1}). */
+int64_t orc_count(int64_t H, int64_t W, int32_t h, int32_t w, int64_t i, int64_t j) {
+  int64_t l, r, o, u;
+  offsets(h, w, &l, &r, &o, &u);
+  return (mn(j + r, W - 1) - mx(j - l, -1)) * (mn(i + u, H - 1) - mx(i - o, -1));
+}
+
+/* Direct window sums, PAPER.md:27 (rows i-h/2 < a <= i+h/2 with the floors of
+ * Alg. 1: rows (i-o, i+u], cols (j-l, j+r]); out-of-bounds terms are zero
+ * (PAPER.md:83), i.e. only in-bounds pixels contribute. */
+static void direct_sums(const uint8_t *I, int64_t H, int64_t W, int64_t pitch, int32_t h, int32_t w,
+                        int64_t i, int64_t j, uint64_t *c, uint64_t *d) {
+  int64_t l, r, o, u;
+  offsets(h, w, &l, &r, &o, &u);
+  uint64_t sc = 0, sd = 0;
+  for (int64_t a = i - o + 1; a <= i + u; ++a) {
+    if (a < 0 || a >= H) continue; /* undefined element = 0 */
+    const uint8_t *row = I + a * pitch;
+    for (int64_t b = j - l + 1; b <= j + r; ++b) {
+      if (b < 0 || b >= W) continue;
+      uint64_t x = row[b];
+      sc += x;
+      sd += x * x;
+    }
+  }
+  *c = sc;
+  *d = sd;
+}
+
+/* Canonical fp64 threshold: Alg. 1 l.121-122 (m = c/n, v = d/n - m^2),
+ * v clamped at 0 (SPEC sweep_mean_variance; never fires for n <= 66049, see
+ * DESIGN.md), s = sqrt(v), then the Table 1 row written left to right:
+ *   Niblack  t = m + k s
+ *   Sauvola  t = m (1 + k (s/R - 1))
+ *   Wolf     t = m - k (m - L)(1 - s/R)       (L = global min PAPER.md:163)
+ */
+double orc_threshold(int32_t method, uint64_t c, uint64_t d, uint64_t n, double k, double R, double L) {
+  double m = (double)c / (double)n;
+  double v = (double)d / (double)n - m * m;
+  if (v < 0) v = 0;
+  double s = sqrt(v);
+  switch (method) {
+    case ORC_SAUVOLA: return m * (1.0 + k * (s / R - 1.0));
+    case ORC_NIBLACK: return m + k * s;
+    case ORC_WOLF: return m - k * (m - L) * (1.0 - s / R);
+  }
+  return NAN;
+}
+
+/* Global minimum of gray levels, Table 1 notation L. */
+int32_t orc_global_min(const uint8_t *I, int64_t H, int64_t W, int64_t pitch) {
+  int32_t L = 255;
+  for (int64_t i = 0; i < H; ++i)
+    for (int64_t j = 0; j < W; ++j)
+      if (I[i * pitch + j] < L) L = I[i * pitch + j];
+  return L;
+}
+
+/* Full binarization by the definition.  mask[i*W+j] = 0 if I <= t (foreground,
+ * Alg. 1 l.124 "I'_ij <- 0"), else 1.  Optional outputs (NULL to skip):
+ * c, d (uint64), n (uint64), t (double).  near_tie counts |I - t| < 1e-9
+ * (BASELINE.json north_star).  Returns 0. */
+int orc_binarize(int32_t method, const uint8_t *I, int64_t H, int64_t W, int64_t pitch, int32_t h, int32_t w,
+                 double k, double R, int32_t L_override, uint8_t *mask, uint64_t *c_out, uint64_t *d_out,
+                 uint64_t *n_out, double *t_out, uint64_t *near_tie) {
+  double L = 0.0;
+  if (method == ORC_WOLF) L = (double)(L_override >= 0 ? L_override : orc_global_min(I, H, W, pitch));
+  uint64_t ties = 0;
+#pragma omp parallel for schedule(static) reduction(+ : ties)
+  for (int64_t i = 0; i < H; ++i) {
+    for (int64_t j = 0; j < W; ++j) {
+      uint64_t c, d;
+      direct_sums(I, H, W, pitch, h, w, i, j, &c, &d);
+      uint64_t n = (uint64_t)orc_count(H, W, h, w, i, j);
+      double t = orc_threshold(method, c, d, n, k, R, L);
+      double x = (double)I[i * pitch + j];
+      if (mask) mask[i * W + j] = (x <= t) ? 0 : 1;
+      if (fabs(x - t) < 1e-9) ties++;
+      if (c_out) c_out[i * W + j] = c;
+      if (d_out) d_out[i * W + j] = d;
+      if (n_out) n_out[i * W + j] = n;
+      if (t_out) t_out[i * W + j] = t;
+    }
+  }
+  if (near_tie) *near_tie = ties;
+  return 0;
+}
+
+/* The same definition evaluated at m sampled positions (rows[k], cols[k]) of
+ * a (possibly huge) page: used for parity at the bench's full sizes. */
+int orc_binarize_points(int32_t method, const uint8_t *I, int64_t H, int64_t W, int64_t pitch, int32_t h,
+                        int32_t w, double k, double R, int32_t L, int64_t m, const int64_t *rows,
+                        const int64_t *cols, uint8_t *mask, uint64_t *c_out, uint64_t *d_out, uint64_t *n_out,
+                        double *t_out) {
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t q = 0; q < m; ++q) {
+    int64_t i = rows[q], j = cols[q];
+    uint64_t c, d;
+    direct_sums(I, H, W, pitch, h, w, i, j, &c, &d);
+    uint64_t n = (uint64_t)orc_count(H, W, h, w, i, j);
+    double t = orc_threshold(method, c, d, n, k, R, (double)L);
+    double x = (double)I[i * pitch + j];
+    if (mask) mask[q] = (x <= t) ? 0 : 1;
+    if (c_out) c_out[q] = c;
+    if (d_out) d_out[q] = d;
+    if (n_out) n_out[q] = n;
+    if (t_out) t_out[q] = t;
+  }
+  return 0;
+}
+
+/* ---- Algorithm 1, transcribed -------------------------
+ * The paper's recursion for c, d, with its own loop structure: column
+ * accumulators C_j, D_j initialised over rows 0..u-1 (l.98-105), updated by
+ * "C_j <- C_j + I_{i+u,j} - I_{i-o,j}" (l.107-110), row accumulators reset
+ * and prefilled with C_0..C_{r-1} (l.111-116), then slid with
+ * "c <- c + C_{j+r} - C_{j-l}" (l.119-120).  Out-of-range reads are zero
+ * (PAPER.md:83).  Outputs c, d per pixel (u64); n from l.118.  Used only as
+ * a pin ("decomposition invariance") and as the paper-method timing. */
+static uint64_t Iz(const uint8_t *I, int64_t H, int64_t W, int64_t pitch, int64_t i, int64_t j) {
+  if (i < 0 || i >= H || j < 0 || j >= W) return 0;
+  return I[i * pitch + j];
+}
+
+int orc_alg1_stats(const uint8_t *I, int64_t H, int64_t W, int64_t pitch, int32_t h, int32_t w, uint64_t *c_out,
+                   uint64_t *d_out) {
+  int64_t l, r, o, u;
+  offsets(h, w, &l, &r, &o, &u);
+  uint64_t *C = (uint64_t *)calloc((size_t)W, sizeof(uint64_t));
+  uint64_t *D = (uint64_t *)calloc((size_t)W, sizeof(uint64_t));
+  if (!C || !D) { free(C); free(D); return -1; }
+  for (int64_t j = 0; j < W; ++j) {
+    C[j] = 0;
+    D[j] = 0;
+    for (int64_t i = 0; i <= u - 1; ++i) {
+      uint64_t x = Iz(I, H, W, pitch, i, j);
+      C[j] += x;
+      D[j] += x * x;
+    }
+  }
+  for (int64_t i = 0; i < H; ++i) {
+    for (int64_t j = 0; j < W; ++j) {
+      uint64_t a = Iz(I, H, W, pitch, i + u, j), b = Iz(I, H, W, pitch, i - o, j);
+      C[j] = C[j] + a - b;
+      D[j] = D[j] + a * a - b * b;
+    }
+    uint64_t c = 0, d = 0;
+    for (int64_t j = 0; j <= r - 1; ++j) {
+      c += (j < W) ? C[j] : 0;
+      d += (j < W) ? D[j] : 0;
+    }
+    for (int64_t j = 0; j < W; ++j) {
+      int64_t jr = j + r, jl = j - l;
+      c = c + ((jr < W) ? C[jr] : 0) - ((jl >= 0) ? C[jl] : 0);
+      d = d + ((jr < W) ? D[jr] : 0) - ((jl >= 0) ? D[jl] : 0);
+      c_out[i * W + j] = c;
+      d_out[i * W + j] = d;
+    }
+  }
+  free(C);
+  free(D);
+  return 0;
+}
+
+/* ---- Sec. 2 integral images -------------------------------
+ * J_{i,j} = J_{i-1,j} + J_{i,j-1} + f(I_{i,j}) - J_{i-1,j-1}, J = 0 for i<0
+ * or j<0; window sum = J_{a1,b1} - J_{a0,b1} - J_{a1,b0} + J_{a0,b0}. */
+int orc_integral_stats(const uint8_t *I, int64_t H, int64_t W, int64_t pitch, int32_t h, int32_t w,
+                       uint64_t *c_out, uint64_t *d_out) {
+  int64_t l, r, o, u;
+  offsets(h, w, &l, &r, &o, &u);
+  uint64_t *J1 = (uint64_t *)malloc((size_t)(H * W) * sizeof(uint64_t));
+  uint64_t *J2 = (uint64_t *)malloc((size_t)(H * W) * sizeof(uint64_t));
+  if (!J1 || !J2) { free(J1); free(J2); return -1; }
+#define JV(J, a, b) (((a) < 0 || (b) < 0) ? 0 : (J)[(a) * W + (b)])
+  for (int64_t i = 0; i < H; ++i)
+    for (int64_t j = 0; j < W; ++j) {
+      uint64_t x = I[i * pitch + j];
+      J1[i * W + j] = JV(J1, i - 1, j) + JV(J1, i, j - 1) + x - JV(J1, i - 1, j - 1);
+      J2[i * W + j] = JV(J2, i - 1, j) + JV(J2, i, j - 1) + x * x - JV(J2, i - 1, j - 1);
+    }
+  for (int64_t i = 0; i < H; ++i)
+    for (int64_t j = 0; j < W; ++j) {
+      int64_t a0 = mx(i - o, -1), a1 = mn(i + u, H - 1), b0 = mx(j - l, -1), b1 = mn(j + r, W - 1);
+      c_out[i * W + j] = JV(J1, a1, b1) - JV(J1, a0, b1) - JV(J1, a1, b0) + JV(J1, a0, b0);
+      d_out[i * W + j] = JV(J2, a1, b1) - JV(J2, a0, b1) - JV(J2, a1, b0) + JV(J2, a0, b0);
+    }
+#undef JV
+  free(J1);
+  free(J2);
+  return 0;
+}
+
+/* ---- Local quantile (rank convention SPEC sweep_quantile) --
+ * Gather the in-bounds window (out-of-bounds pixels are excluded, not zero
+ * padded: the quantile is of the n gray levels that exist), sort, and take
+ * the rho-th smallest, rho = max(1, ceil(q n)).  mask = 0 iff I <= Q. */
+static int cmp_u8(const void *a, const void *b) { return (int)*(const uint8_t *)a - (int)*(const uint8_t *)b; }
+
+static uint8_t direct_quantile(const uint8_t *I, int64_t H, int64_t W, int64_t pitch, int32_t h, int32_t w,
+                               double q, int64_t i, int64_t j, uint8_t *buf) {
+  int64_t l, r, o, u;
+  offsets(h, w, &l, &r, &o, &u);
+  int64_t n = 0;
+  for (int64_t a = i - o + 1; a <= i + u; ++a) {
+    if (a < 0 || a >= H) continue;
+    for (int64_t b = j - l + 1; b <= j + r; ++b) {
+      if (b < 0 || b >= W) continue;
+      buf[n++] = I[a * pitch + b];
+    }
+  }
+  qsort(buf, (size_t)n, 1, cmp_u8);
+  int64_t rho = (int64_t)ceil(q * (double)n);
+  if (rho < 1) rho = 1;
+  return buf[rho - 1];
+}
+
+int orc_quantile(const uint8_t *I, int64_t H, int64_t W, int64_t pitch, int32_t h, int32_t w, double q,
+                 uint8_t *mask, uint8_t *Q_out) {
+  int rc = 0;
+#pragma omp parallel
+  {
+    uint8_t *buf = (uint8_t *)malloc((size_t)mn(h, H) * (size_t)mn(w, W));
+    if (!buf) {
+#pragma omp atomic write
+      rc = -1;
+    } else {
+#pragma omp for schedule(static)
+      for (int64_t i = 0; i < H; ++i)
+        for (int64_t j = 0; j < W; ++j) {
+          uint8_t Q = direct_quantile(I, H, W, pitch, h, w, q, i, j, buf);
+          if (Q_out) Q_out[i * W + j] = Q;
+          if (mask) mask[i * W + j] = (I[i * pitch + j] <= Q) ? 0 : 1;
+        }
+      free(buf);
+    }
+  }
+  return rc;
+}
+
+int orc_quantile_points(const uint8_t *I, int64_t H, int64_t W, int64_t pitch, int32_t h, int32_t w, double q,
+                        int64_t m, const int64_t *rows, const int64_t *cols, uint8_t *mask, uint8_t *Q_out) {
+  int rc = 0;
+#pragma omp parallel
+  {
+    uint8_t *buf = (uint8_t *)malloc((size_t)mn(h, H) * (size_t)mn(w, W));
+    if (!buf) {
+#pragma omp atomic write
+      rc = -1;
+    } else {
+#pragma omp for schedule(dynamic, 64)
+      for (int64_t p = 0; p < m; ++p) {
+        uint8_t Q = direct_quantile(I, H, W, pitch, h, w, q, rows[p], cols[p], buf);
+        if (Q_out) Q_out[p] = Q;
+        if (mask) mask[p] = (I[rows[p] * pitch + cols[p]] <= Q) ? 0 : 1;
+      }
+      free(buf);
+    }
+  }
+  return rc;
+}

@@ -1,0 +1,339 @@
+"""Pins for the CPU oracle (-m "not gpu").
+
+The oracle (oracle/abin_oracle.c) is checked against things other than its
+own formulas: the paper's real-valued window bounds by brute
+force, SPEC.md's worked values (tests/golden/spec_examples.json), closed
+forms (constant images, 1x1 windows, whole-image windows), the paper's
+accumulator bounds, exact-rational evaluation of Algorithm 1's
+square-root-free condition, the two other engines the
+paper names (Alg. 1 recursion PAPER.md:98-120, integral images PAPER.md:48),
+and symmetry invariants (transposition, flips for odd windows).
+"""
+import json
+import math
+import os
+import subprocess
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+# ---------------------------------------------------------------- brute force
+
+def brute_window(H, W, h, w, i, j):
+    """In-bounds (a, b) with i - h/2 < a <= i + h/2 and j - w/2 < b <= j + w/2,
+    the real-valued bounds of PAPER.md:27 (Fractions, no floors)."""
+    hh, ww = Fraction(h, 2), Fraction(w, 2)
+    rows = [a for a in range(H) if i - hh < a <= i + hh]
+    cols = [b for b in range(W) if j - ww < b <= j + ww]
+    return rows, cols
+
+
+def brute_stats(I, h, w, i, j):
+    H, W = I.shape
+    rows, cols = brute_window(H, W, h, w, i, j)
+    vals = [int(I[a, b]) for a in rows for b in cols]
+    return sum(vals), sum(v * v for v in vals), len(vals), vals
+
+
+# ---------------------------------------------------------------- offsets, n
+
+def test_offsets_spec_examples():
+    for ex in GOLD["offsets"]:
+        l, r, _, _ = oracle.offsets(1, ex["w"])
+        assert (l, r) == (ex["l"], ex["r"]), ex["cite"]
+
+
+def test_offsets_match_paper_real_bounds():
+    # Alg. 1's floors describe exactly the real-valued window
+    # of PAPER.md:27: {b : j - w/2 < b <= j + w/2} == (j - l, j + r].
+    for w in range(1, 40):
+        l, r, o, u = oracle.offsets(w, w)
+        assert (l, r) == (o, u)
+        for j in range(-3, 4):
+            real = [b for b in range(j - 50, j + 50) if j - Fraction(w, 2) < b <= j + Fraction(w, 2)]
+            assert real == list(range(j - l + 1, j + r + 1))
+            assert len(real) == w
+
+
+def test_count_spec_examples():
+    for ex in GOLD["count"]:
+        assert oracle.count(ex["H"], ex["W"], ex["h"], ex["w"], ex["i"], ex["j"]) == ex["n"], ex["cite"]
+
+
+def test_count_equals_brute_enumeration():
+    rng = np.random.default_rng(1)
+    for _ in range(400):
+        H, W = rng.integers(1, 30, size=2)
+        h, w = rng.integers(1, 70, size=2)
+        i, j = rng.integers(0, H), rng.integers(0, W)
+        rows, cols = brute_window(H, W, h, w, i, j)
+        assert oracle.count(H, W, h, w, i, j) == len(rows) * len(cols) >= 1
+
+
+# ---------------------------------------------------------------- window sums
+
+SPEC_WINDOWS = [(1, 1), (2, 2), (3, 3), (2, 5), (5, 2), (31, 31), (64, 64), (100, 7)]
+
+
+def test_sums_equal_brute_force_tiny():
+    rng = np.random.default_rng(2)
+    for trial in range(12):
+        H, W = rng.integers(1, 13, size=2)
+        I = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+        for (h, w) in [(1, 1), (2, 3), (3, 2), (4, 4), (5, 7), (13, 2), (30, 30)]:
+            r = oracle.binarize("sauvola", I, h, w, 0.5, 128.0, stats=True)
+            for i in range(H):
+                for j in range(W):
+                    c, d, n, _ = brute_stats(I, h, w, i, j)
+                    assert (r["c"][i, j], r["d"][i, j], r["n"][i, j]) == (c, d, n)
+
+
+@pytest.mark.parametrize("hw", SPEC_WINDOWS)
+def test_decomposition_invariance(hw):
+    # direct == Algorithm 1 recursion ==
+    # integral images, exactly, on the SPEC grid of windows.
+    h, w = hw
+    rng = np.random.default_rng(h * 1000 + w)
+    shapes = [(1, 1), (7, 9), (33, 20), (3, 200), (200, 3), (64, 64)]
+    for H, W in shapes:
+        I = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+        r = oracle.binarize("niblack", I, h, w, -0.2, 128.0, stats=True)
+        c1, d1 = oracle.alg1_stats(I, h, w)
+        c2, d2 = oracle.integral_stats(I, h, w)
+        assert np.array_equal(r["c"], c1) and np.array_equal(r["d"], d1)
+        assert np.array_equal(r["c"], c2) and np.array_equal(r["d"], d2)
+
+
+def test_paper_accumulator_bounds():
+    # all-255 image, window side 257 -> max C = 65535 and
+    # max D = 255^2 * 257 = 16,711,425 (a 257 x 1 window is one column sum).
+    b = GOLD["bounds"]
+    I = np.full((300, 3), 255, np.uint8)
+    r = oracle.binarize("sauvola", I, b["h"], 1, 0.5, 128.0, stats=True)
+    assert int(r["c"].max()) == b["maxC"] and int(r["d"].max()) == b["maxD"]
+
+
+def test_centre255_spec_example():
+    g = GOLD["centre255"]
+    I = np.array(g["image"], np.uint8)
+    r = oracle.binarize("sauvola", I, g["h"], g["w"], 0.5, 128.0, stats=True)
+    assert (r["c"][1, 1], r["d"][1, 1], r["n"][1, 1]) == (g["c"], g["d"], g["n"])
+    m = Fraction(255, 9)
+    v = Fraction(255 ** 2, 9) - m * m
+    t_exact = float(m) * (1 + 0.5 * (math.sqrt(float(v)) / 128.0 - 1))
+    assert abs(r["t"][1, 1] - t_exact) <= 1e-12 * abs(t_exact)
+
+
+# ---------------------------------------------------------------- thresholds
+
+def test_threshold_spec_examples():
+    for ex in GOLD["threshold"]:
+        t = oracle.threshold(ex["method"], ex["c"], ex["d"], ex["n"], ex["k"], ex["R"], ex["L"])
+        assert abs(t - ex["t"]) <= 1e-12 * abs(ex["t"]), ex["cite"]
+
+
+def test_decide_spec_examples():
+    for ex in GOLD["decide"]:
+        I = np.full((3, 3), ex["g"], np.uint8)
+        mask = oracle.binarize(ex["method"], I, 3, 3, ex["k"], ex["R"])
+        assert mask[1, 1] == ex["mask"], ex["cite"]
+
+
+@pytest.mark.parametrize("g", [0, 1, 77, 128, 200, 255])
+def test_constant_image_closed_forms(g):
+    # Constant image: v = 0 exactly, Sauvola t = g (1 - k) (north star),
+    # Niblack t = g (an exact tie: all foreground, every pixel a near-tie).
+    I = np.full((9, 11), g, np.uint8)
+    for k in (0.5, 0.34, 0.2):
+        r = oracle.binarize("sauvola", I, 4, 5, k, 128.0, stats=True)
+        assert np.all(np.abs(r["t"] - g * (1 - k)) <= 1e-12 * max(g, 1))
+        assert np.all(r["mask"] == (0 if g == 0 else 1))
+    r = oracle.binarize("niblack", I, 4, 5, -0.2, 128.0, stats=True)
+    assert np.all(r["t"] == g) and np.all(r["mask"] == 0) and r["near_tie"] == I.size
+
+
+def test_one_by_one_window():
+    # h = w = 1: n = 1, v = 0, Sauvola t = I (1 - k): foreground only where I = 0.
+    I = synth.uniform_random(17, 23, 5)
+    I[0, :5] = 0
+    m = oracle.binarize("sauvola", I, 1, 1, 0.5, 128.0)
+    assert np.array_equal(m, (I != 0).astype(np.uint8))
+
+
+def test_whole_image_window_is_global_threshold():
+    # A window covering the whole image from every pixel (h >= 2H-1, w >= 2W-1)
+    # gives m = global mean, v = global variance at every pixel (north star).
+    I = synth.uniform_random(13, 9, 7)
+    vals = [int(x) for x in I.ravel()]
+    N = len(vals)
+    m = Fraction(sum(vals), N)
+    v = Fraction(sum(x * x for x in vals), N) - m * m
+    for method, k in (("sauvola", 0.5), ("niblack", -0.2), ("wolf", 0.5)):
+        r = oracle.binarize(method, I, 2 * 13 - 1, 2 * 9 - 1, k, 128.0, stats=True)
+        assert np.all(r["c"] == sum(vals)) and np.all(r["n"] == N)
+        s = math.sqrt(float(v))
+        L = min(vals)
+        t_ref = {"sauvola": float(m) * (1 + k * (s / 128 - 1)), "niblack": float(m) + k * s,
+                 "wolf": float(m) - k * (float(m) - L) * (1 - s / 128)}[method]
+        assert np.all(np.abs(r["t"] - t_ref) <= 1e-12 * abs(t_ref))
+
+
+def test_sauvola_and_wolf_reduce_to_mean_when_s_equals_R():
+    # Table 1: with s = R, Sauvola m(1 + k(1 - 1)) = m and Wolf m - k(m-L)*0 = m.
+    # Window {0, 255}: m = 127.5, s = 127.5 exactly; choose R = 127.5.
+    for method in ("sauvola", "wolf"):
+        t = oracle.threshold(method, 255, 255 * 255, 2, 0.5, 127.5, 0.0)
+        assert t == 127.5
+    # Wolf with L = m: t = m for any s.
+    assert oracle.threshold("wolf", 300, 10 ** 5, 3, 0.5, 128.0, 100.0) == 100.0
+
+
+def _sqrt_free_decision(I, c, d, n, k, R):
+    """Alg. 1 l.124 condition in exact rationals (k >= 0):
+    I + m(k-1) <= 0  or  (I + m(k-1))^2 <= k^2 m^2 v / R^2."""
+    m = Fraction(c, n)
+    v = Fraction(d, n) - m * m
+    k, R = Fraction(k), Fraction(R)
+    a = I + m * (k - 1)
+    return 0 if (a <= 0 or a * a <= k * k * m * m * v / (R * R)) else 1
+
+
+def _exact_gap(I, c, d, n, k, R):
+    m = Fraction(c, n)
+    v = Fraction(d, n) - m * m
+    return abs(I - float(m) * (1 + k * (math.sqrt(float(v)) / R - 1)))
+
+
+def test_sqrt_free_equivalence():
+    # I <= m(1 + k(s/R - 1)) <=> Alg. 1's square-root-free test
+    # (k >= 0).  The oracle's explicit-t decision must agree with the exact
+    # rational square-root-free decision off near-ties (SPEC acceptance 8).
+    rng = np.random.default_rng(8)
+    checked = 0
+    for _ in range(20000):
+        n = int(rng.integers(1, 400))
+        vals = rng.integers(0, 256, size=n)
+        c, d = int(vals.sum()), int((vals.astype(np.int64) ** 2).sum())
+        I = int(rng.integers(0, 256))
+        k = float(rng.choice([0.0, 0.1, 0.34, 0.5, 0.9, 1.5]))
+        R = float(rng.choice([64.0, 128.0, 200.0]))
+        if _exact_gap(I, c, d, n, k, R) < 1e-6:
+            continue
+        t = oracle.threshold("sauvola", c, d, n, k, R)
+        assert (0 if I <= t else 1) == _sqrt_free_decision(I, c, d, n, k, R)
+        checked += 1
+    assert checked > 19000
+
+
+def test_fp64_threshold_within_bound_of_exact():
+    # |t_fp64 - t*| stays far below the 1e-9 near-tie band (R3):
+    # compare with a high-precision evaluation from the exact integers.
+    from decimal import Decimal, getcontext
+    getcontext().prec = 50
+    rng = np.random.default_rng(9)
+    for _ in range(3000):
+        n = int(rng.integers(2, 66049))
+        lo = int(rng.integers(0, 250))
+        spread = int(rng.integers(1, 6))
+        m_ = int(rng.integers(1, 2000))
+        vals = rng.integers(lo, lo + spread + 1, size=min(n, m_))
+        n = vals.size
+        c, d = int(vals.sum()), int((vals.astype(np.int64) ** 2).sum())
+        V = n * d - c * c
+        k, R = -0.2, 128.0
+        sD = Decimal(V).sqrt() / Decimal(n)
+        t_star = Decimal(c) / Decimal(n) + Decimal(k) * sD
+        t = oracle.threshold("niblack", c, d, n, k, R)
+        assert abs(Decimal(t) - t_star) < Decimal("1e-10")
+
+
+# ---------------------------------------------------------------- symmetry
+
+def test_transposition_invariance():
+    # PAPER.md:134 (axis exchange): bin(I^T; h<->w) == bin(I)^T.
+    I = synth.page(40, 57, 11)
+    for (h, w) in [(5, 9), (8, 3), (32, 32), (61, 2)]:
+        for method, k in (("sauvola", 0.5), ("niblack", -0.2), ("wolf", 0.5)):
+            a = oracle.binarize(method, I, h, w, k, 128.0, stats=True)
+            b = oracle.binarize(method, np.ascontiguousarray(I.T), w, h, k, 128.0, stats=True)
+            assert np.array_equal(a["mask"], b["mask"].T)
+            assert np.array_equal(a["t"], b["t"].T)
+
+
+def test_flip_invariance_only_for_odd_windows():
+    I = synth.uniform_random(23, 31, 12)
+    flip = np.ascontiguousarray(I[:, ::-1])
+    a = oracle.binarize("sauvola", I, 5, 7, 0.5, 128.0, stats=True)
+    b = oracle.binarize("sauvola", flip, 5, 7, 0.5, 128.0, stats=True)
+    assert np.array_equal(a["c"], b["c"][:, ::-1])
+    # even w is asymmetric, (j - w/2, j + w/2]: the flipped stats differ
+    a = oracle.binarize("sauvola", I, 5, 6, 0.5, 128.0, stats=True)
+    b = oracle.binarize("sauvola", flip, 5, 6, 0.5, 128.0, stats=True)
+    assert not np.array_equal(a["c"], b["c"][:, ::-1])
+
+
+def test_wolf_uses_global_min():
+    I = synth.uniform_random(20, 20, 3, lo=40, hi=220)
+    L = oracle.global_min(I)
+    assert L == int(I.min())
+    a = oracle.binarize("wolf", I, 7, 7, 0.5, 128.0, stats=True)
+    b = oracle.binarize("wolf", I, 7, 7, 0.5, 128.0, L=L, stats=True)
+    assert np.array_equal(a["t"], b["t"])
+
+
+# ---------------------------------------------------------------- quantiles
+
+def test_quantile_spec_median():
+    g = GOLD["median"]
+    I = np.array(g["image"], np.uint8)
+    _, Q = oracle.quantile(I, g["h"], g["w"], g["q"])
+    assert Q[0, 1] == g["Q_centre"], g["cite"]
+
+
+def test_quantile_brute_force_and_special_cases():
+    rng = np.random.default_rng(13)
+    for _ in range(6):
+        H, W = rng.integers(1, 14, size=2)
+        I = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+        for (h, w) in [(1, 1), (3, 3), (4, 5), (5, 5), (30, 2)]:
+            for q in (0.1, 0.5, 0.9, 1.0, 1e-6):
+                mask, Q = oracle.quantile(I, h, w, q)
+                for i in range(H):
+                    for j in range(W):
+                        _, _, n, vals = brute_stats(I, h, w, i, j)
+                        s = sorted(vals)
+                        if q == 1.0:
+                            assert Q[i, j] == s[-1]          # q = 1: window max
+                        if q == 1e-6:
+                            assert Q[i, j] == s[0]           # rho = 1: window min
+                        if q == 0.5 and n % 2 == 1:
+                            assert Q[i, j] == int(np.median(vals))  # odd n: the median
+                        # rank convention: #(x <= Q) >= rho > #(x < Q)
+                        rho = max(1, math.ceil(Fraction(str(q)) * n)) if q != 1e-6 else 1
+                        assert sum(x <= Q[i, j] for x in vals) >= rho > sum(x < Q[i, j] for x in vals)
+                        assert mask[i, j] == (0 if I[i, j] <= Q[i, j] else 1)
+
+
+def test_quantile_monotone_in_q():
+    I = synth.page(30, 40, 21)
+    prev = None
+    for q in (0.1, 0.25, 0.5, 0.75, 0.9, 1.0):
+        _, Q = oracle.quantile(I, 7, 9, q)
+        if prev is not None:
+            assert np.all(Q >= prev)
+        prev = Q
+
+
+# ---------------------------------------------------------------- build guard
+
+def test_oracle_compiled_without_fma_contraction():
+    # The canonical double sequence must not be contracted into FMAs.
+    out = subprocess.run(["objdump", "-d", oracle.build()], capture_output=True, text=True).stdout
+    assert "vfmadd" not in out and "vfmsub" not in out and "vfnmadd" not in out
