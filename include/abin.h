@@ -1,0 +1,176 @@
+/*
+ * abin.h -- C ABI of libabin.so, the B200 (sm_100a) hot path of
+ * Chan, "Memory-efficient and fast implementation of local adaptive
+ * binarization methods", arXiv 1905.13038.
+ *
+ * What every binarization entry point computes (the paper's definitions):
+ *
+ *   window      rows (i-o, i+u], cols (j-l, j+r] with
+ *               l = floor((w+1)/2), r = floor(w/2), o = floor((h+1)/2),
+ *               u = floor(h/2)                      -- Alg. 1 l.1-4
+ *   sums        c = sum I, d = sum I^2 over the in-bounds part of the window
+ *               (undefined elements are zero)      -- PAPER.md:27, 83
+ *   count       n = (min{j+r,W-1} - max{j-l,-1}) * (min{i+u,H-1} - max{i-o,-1})
+ *                                                   -- Alg. 1 l.118
+ *   moments     m = c/n, v = d/n - m^2 (clamped at 0), s = sqrt(v)
+ *                                                   -- Alg. 1 l.121-122
+ *   threshold   Sauvola t = m (1 + k (s/R - 1))     -- PAPER.md:24, Table 1 (l.152)
+ *               Niblack t = m + k s                 -- Table 1
+ *               Wolf    t = m - k (m - L)(1 - s/R), L = global minimum
+ *                                                   -- Table 1
+ *   decision    I' = 0 (foreground) if I <= t, else 1 -- Alg. 1 l.124
+ *
+ * t is evaluated in IEEE double, left to right, with no FMA contraction, so
+ * the mask is bit-identical to a plain CPU evaluation of the same formula.
+ * (The kernels decide most pixels with a certified fp32 bound and re-evaluate
+ * the ambiguous ones in that exact double sequence.)
+ *
+ * abin_quantile computes, per pixel, Q = the rho-th smallest in-bounds gray
+ * level of the window, rho = max(1, ceil(q n)), and I' = 0 iff I <= Q
+ * (local quantiles via sliding histograms).
+ *
+ * Conventions shared by all entry points
+ * -------------------------------------
+ * - Images are uint8, row-major, `H` rows of `W` pixels, rows `pitch` bytes
+ *   apart (pitch >= W).  Page batches place page p at `in + p*in_page_stride`.
+ * - All image / mask pointers are DEVICE pointers (cudaMalloc'd or torch CUDA
+ *   tensors) unless the flag ABIN_HOST_IO is given (abin_*_batched only): then
+ *   `in` and `out` are HOST pointers (pinned memory recommended) and the
+ *   library streams pages through device staging buffers it owns.
+ * - The caller owns every buffer.  Input and output must not overlap
+ *   (the in-place variant is out of scope) -> ABIN_EALIAS.
+ * - Output mask formats: ABIN_MASK_U8: one byte per pixel, value 0 or 1,
+ *   row stride out_pitch >= W.  ABIN_MASK_BITS: one bit per pixel,
+ *   MSB-first (pixel j -> byte j>>3, bit 7-(j&7)), bit = I', rows padded with
+ *   0 bits to whole bytes, out_pitch >= ceil(W/8).
+ * - Work is enqueued asynchronously on `stream` (a cudaStream_t; NULL = the
+ *   legacy default stream).  The call returns once the work is enqueued;
+ *   asynchronous device faults surface at the caller's next synchronisation.
+ *   Entry points are reentrant across streams.
+ * - `counters` (optional, device pointer to 2 x uint64, may be NULL):
+ *   counters[0] += pixels with |I - t| < 1e-9 ("near ties"),
+ *   counters[1] += pixels the certified fp32 filter sent to the exact fp64
+ *   path.  Accumulated with device atomics; the caller zeroes them.
+ * - Windows: any h, w >= 1 are legal, including windows larger than the
+ *   image (SPEC window-geometry); even sizes are asymmetric per the floors.
+ *
+ * Error behaviour: every entry point validates its arguments before touching
+ * the device and returns one of abin_status; nothing is enqueued on error.
+ */
+#ifndef ABIN_H
+#define ABIN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ABIN_VERSION_MAJOR 0
+#define ABIN_VERSION_MINOR 1
+
+typedef enum {
+  ABIN_OK = 0,
+  ABIN_EINVAL = 1, /* null pointer, H/W/h/w < 1, pitch too small, non-finite k/R, R <= 0, q not in (0,1], bad format */
+  ABIN_EALIAS = 2, /* input and output byte ranges overlap */
+  ABIN_ERANGE = 3, /* window or image exceeds what the kernels support (see abin_limits) */
+  ABIN_ECUDA = 4,  /* a CUDA runtime call or launch failed */
+  ABIN_ENOMEM = 5  /* ABIN_HOST_IO staging allocation failed */
+} abin_status;
+
+enum { ABIN_MASK_U8 = 0, ABIN_MASK_BITS = 1 };
+
+enum {
+  ABIN_FORCE_U64_SQ = 1u << 0, /* accumulate window square sums d in uint64 even when uint32 is exact */
+  ABIN_FORCE_FP64 = 1u << 1,   /* skip the fp32 filter: every pixel takes the exact fp64 sequence */
+  ABIN_HOST_IO = 1u << 2       /* (batched calls) in/out are host pointers; copies are part of the call */
+};
+
+/* ---- Sauvola (Table 1) --------------------------------------
+ * in        device uint8 image, H x W, row pitch in_pitch bytes
+ * out       device mask, row pitch out_pitch bytes, format mask_format
+ * h, w      window height / width (>= 1)
+ * k, R      Sauvola parameters (finite; R > 0).  The paper uses k = 0.5, R = 128.
+ */
+int abin_sauvola(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out, int64_t out_pitch,
+                 int32_t mask_format, int32_t h, int32_t w, double k, double R, uint32_t flags,
+                 uint64_t* counters, void* stream);
+
+/* ---- Niblack (Table 1); k may be negative (e.g. -0.2) ------- */
+int abin_niblack(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out, int64_t out_pitch,
+                 int32_t mask_format, int32_t h, int32_t w, double k, uint32_t flags, uint64_t* counters,
+                 void* stream);
+
+/* ---- Wolf (Table 1) ------------------------------------------
+ * L_override < 0: L is the page's global minimum gray level, computed on the
+ * device (abin_global_min) without a host round trip.  L_override in 0..255
+ * uses that value (band mode: pass the minimum over the WHOLE image). */
+int abin_wolf(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out, int64_t out_pitch,
+              int32_t mask_format, int32_t h, int32_t w, double k, double R, int32_t L_override, uint32_t flags,
+              uint64_t* counters, void* stream);
+
+/* ---- Local quantile threshold -------------------------------
+ * q in (0, 1]: Q = rho-th smallest in-bounds level, rho = max(1, ceil(q n)).
+ * q = 0.5 is the (lower) local median. */
+int abin_quantile(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out, int64_t out_pitch,
+                  int32_t mask_format, int32_t h, int32_t w, double q, uint32_t flags, void* stream);
+
+/* ---- Page batches ------------------------------------------------------------
+ * n_pages pages of identical H x W geometry; page p is read at
+ * in + p * in_page_stride and written at out + p * out_page_stride (bytes).
+ * method: 0 Sauvola, 1 Niblack, 2 Wolf (per-page L unless L_override >= 0),
+ * 3 quantile (param0 = q).  param0 = k (or q), param1 = R.
+ * With ABIN_HOST_IO, in/out are host pointers. */
+enum { ABIN_SAUVOLA = 0, ABIN_NIBLACK = 1, ABIN_WOLF = 2, ABIN_QUANTILE = 3 };
+int abin_binarize_batched(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8_t* out,
+                          int64_t out_page_stride, int64_t n_pages, int64_t H, int64_t W, int64_t in_pitch,
+                          int64_t out_pitch, int32_t mask_format, int32_t h, int32_t w, double param0,
+                          double param1, int32_t L_override, uint32_t flags, uint64_t* counters, void* stream);
+
+/* ---- Row bands of a larger image (multi-GPU row decomposition) --------------
+ * The caller holds rows [row0 - halo_top, row0 + H_band + halo_bot) of an
+ * image that is H_global rows tall; `in` points at the first held row
+ * (global row row0 - halo_top).  Output rows are the band's own rows
+ * [row0, row0 + H_band); `out` points at the mask row of global row row0.
+ * n and the image-edge convention use the GLOBAL geometry, so the union of
+ * all bands' masks equals the whole-image mask bit for bit, provided
+ * halo_top >= min(o - 1, row0) and halo_bot >= min(u, H_global - row0 - H_band)
+ * (else ABIN_EINVAL).  Wolf needs the global minimum: L_override >= 0 required. */
+int abin_binarize_band(int32_t method, const uint8_t* in, int64_t H_band, int64_t W, int64_t in_pitch,
+                       int64_t row0, int64_t H_global, int32_t halo_top, int32_t halo_bot, uint8_t* out,
+                       int64_t out_pitch, int32_t mask_format, int32_t h, int32_t w, double param0,
+                       double param1, int32_t L_override, uint32_t flags, uint64_t* counters, void* stream);
+
+/* ---- Global minimum L (Table 1 notation) ----------------------
+ * L_out: device uint8[n_pages], the minimum gray level of each page. */
+int abin_global_min(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64_t H, int64_t W,
+                    int64_t in_pitch, uint8_t* L_out, void* stream);
+
+/* ---- Per-pixel statistics (parity / debugging) -------------------------------
+ * Same kernels as the binarization path, additionally storing, per pixel
+ * (row-major, H*W elements each, device pointers, any may be NULL):
+ *   c_out, d_out  uint64 window sums;   n_out uint32 count;
+ *   t_out         double threshold (the exact fp64 sequence, every pixel);
+ *   mask_out      uint8 mask (ABIN_MASK_U8 layout, pitch W).
+ * method 0..2 as above (L_override as for Wolf).  For method 3 (quantile)
+ * t_out receives Q as a double and c_out/d_out are not written. */
+int abin_stats(int32_t method, const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, int32_t h, int32_t w,
+               double param0, double param1, int32_t L_override, uint64_t* c_out, uint64_t* d_out,
+               uint32_t* n_out, double* t_out, uint8_t* mask_out, void* stream);
+
+/* ---- Limits, versions, errors ------------------------------------------------ */
+typedef struct {
+  int64_t max_window_w; /* largest effective window width min(l,W)+min(r,W) the kernels take */
+  int64_t max_window_h; /* largest window height */
+  int64_t max_dim;      /* largest H or W */
+} abin_limits_t;
+void abin_limits(abin_limits_t* out);
+const char* abin_strerror(int status);
+const char* abin_version(void);
+/* Last CUDA error string recorded by a failing call on this thread ("" if none). */
+const char* abin_last_cuda_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ABIN_H */

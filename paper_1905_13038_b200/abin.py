@@ -1,0 +1,213 @@
+"""Thin Python binding of libabin.so (include/abin.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels behind the C ABI.  Tensors are torch CUDA uint8 tensors (device
+memory, streams and process groups are all PyTorch provides here).  There is
+no CPU fallback: if the shared library is missing, importing this module
+raises.
+"""
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libabin.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+_U32 = ctypes.c_uint32
+_D = ctypes.c_double
+
+SAUVOLA, NIBLACK, WOLF, QUANTILE = 0, 1, 2, 3
+METHODS = {"sauvola": SAUVOLA, "niblack": NIBLACK, "wolf": WOLF, "quantile": QUANTILE}
+MASK_U8, MASK_BITS = 0, 1
+FORCE_U64_SQ, FORCE_FP64, HOST_IO = 1, 2, 4
+OK, EINVAL, EALIAS, ERANGE, ECUDA, ENOMEM = 0, 1, 2, 3, 4, 5
+
+_lib.abin_sauvola.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _D, _D, _U32, _P, _P]
+_lib.abin_niblack.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _D, _U32, _P, _P]
+_lib.abin_wolf.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _D, _D, _I32, _U32, _P, _P]
+_lib.abin_quantile.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _D, _U32, _P]
+_lib.abin_binarize_batched.argtypes = [_I32, _P, _I64, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _D,
+                                       _D, _I32, _U32, _P, _P]
+_lib.abin_binarize_band.argtypes = [_I32, _P, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _P, _I64, _I32, _I32, _I32,
+                                    _D, _D, _I32, _U32, _P, _P]
+_lib.abin_global_min.argtypes = [_P, _I64, _I64, _I64, _I64, _I64, _P, _P]
+_lib.abin_stats.argtypes = [_I32, _P, _I64, _I64, _I64, _I32, _I32, _D, _D, _I32, _P, _P, _P, _P, _P, _P]
+_lib.abin_strerror.argtypes = [ctypes.c_int]
+_lib.abin_strerror.restype = ctypes.c_char_p
+_lib.abin_version.restype = ctypes.c_char_p
+_lib.abin_last_cuda_error.restype = ctypes.c_char_p
+
+
+class AbinLimits(ctypes.Structure):
+    _fields_ = [("max_window_w", _I64), ("max_window_h", _I64), ("max_dim", _I64)]
+
+
+_lib.abin_limits.argtypes = [ctypes.POINTER(AbinLimits)]
+
+EXPORTED = ["abin_sauvola", "abin_niblack", "abin_wolf", "abin_quantile", "abin_binarize_batched",
+            "abin_binarize_band", "abin_global_min", "abin_stats", "abin_limits", "abin_strerror", "abin_version",
+            "abin_last_cuda_error"]
+
+
+class AbinError(RuntimeError):
+    def __init__(self, status: int):
+        msg = _lib.abin_strerror(status).decode()
+        if status == ECUDA:
+            msg += ": " + _lib.abin_last_cuda_error().decode()
+        super().__init__(f"abin status {status}: {msg}")
+        self.status = status
+
+
+def _check(rc: int) -> None:
+    if rc != OK:
+        raise AbinError(rc)
+
+
+def version() -> str:
+    return _lib.abin_version().decode()
+
+
+def limits() -> AbinLimits:
+    out = AbinLimits()
+    _lib.abin_limits(ctypes.byref(out))
+    return out
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _img2d(x: torch.Tensor):
+    if x.dtype != torch.uint8 or x.dim() != 2 or not x.is_cuda or x.stride(1) != 1:
+        raise ValueError("expected a 2-D CUDA uint8 tensor with unit column stride")
+    return x.shape[0], x.shape[1], x.stride(0)
+
+
+def _alloc_mask(H, W, packed, device, pitch=None):
+    cols = (W + 7) // 8 if packed else W
+    if pitch is None:
+        return torch.empty((H, cols), dtype=torch.uint8, device=device)
+    buf = torch.empty((H, pitch), dtype=torch.uint8, device=device)
+    return buf[:, :cols]
+
+
+def sauvola(img: torch.Tensor, h: int, w: int, k: float = 0.5, R: float = 128.0, packed: bool = False, out=None,
+            flags: int = 0, counters: torch.Tensor = None, stream=None) -> torch.Tensor:
+    """Sauvola binarization (Table 1): mask 0 = foreground."""
+    H, W, pitch = _img2d(img)
+    out = _alloc_mask(H, W, packed, img.device) if out is None else out
+    _check(_lib.abin_sauvola(_ptr(img), H, W, pitch, _ptr(out), out.stride(0), MASK_BITS if packed else MASK_U8, h,
+                             w, k, R, flags, _ptr(counters), _stream(stream)))
+    return out
+
+
+def niblack(img: torch.Tensor, h: int, w: int, k: float = -0.2, packed: bool = False, out=None, flags: int = 0,
+            counters: torch.Tensor = None, stream=None) -> torch.Tensor:
+    """Niblack binarization (Table 1)."""
+    H, W, pitch = _img2d(img)
+    out = _alloc_mask(H, W, packed, img.device) if out is None else out
+    _check(_lib.abin_niblack(_ptr(img), H, W, pitch, _ptr(out), out.stride(0), MASK_BITS if packed else MASK_U8, h,
+                             w, k, flags, _ptr(counters), _stream(stream)))
+    return out
+
+
+def wolf(img: torch.Tensor, h: int, w: int, k: float = 0.5, R: float = 128.0, L: int = -1, packed: bool = False,
+         out=None, flags: int = 0, counters: torch.Tensor = None, stream=None) -> torch.Tensor:
+    """Wolf binarization (Table 1); L < 0: global min on device."""
+    H, W, pitch = _img2d(img)
+    out = _alloc_mask(H, W, packed, img.device) if out is None else out
+    _check(_lib.abin_wolf(_ptr(img), H, W, pitch, _ptr(out), out.stride(0), MASK_BITS if packed else MASK_U8, h, w, k,
+                          R, L, flags, _ptr(counters), _stream(stream)))
+    return out
+
+
+def quantile(img: torch.Tensor, h: int, w: int, q: float = 0.5, packed: bool = False, out=None, flags: int = 0,
+             stream=None) -> torch.Tensor:
+    """Local-quantile threshold: mask 0 iff I <= Q."""
+    H, W, pitch = _img2d(img)
+    out = _alloc_mask(H, W, packed, img.device) if out is None else out
+    _check(_lib.abin_quantile(_ptr(img), H, W, pitch, _ptr(out), out.stride(0), MASK_BITS if packed else MASK_U8, h,
+                              w, q, flags, _stream(stream)))
+    return out
+
+
+def binarize_batched(method: str, pages: torch.Tensor, h: int, w: int, param0: float, param1: float = 128.0,
+                     L: int = -1, packed: bool = False, out=None, flags: int = 0, counters: torch.Tensor = None,
+                     stream=None) -> torch.Tensor:
+    """P pages (a (P, H, W) uint8 tensor, unit column stride) in one launch."""
+    if pages.dtype != torch.uint8 or pages.dim() != 3 or pages.stride(2) != 1:
+        raise ValueError("expected a (P, H, W) uint8 tensor with unit column stride")
+    P, H, W = pages.shape
+    if out is None:
+        out = torch.empty((P, H, (W + 7) // 8 if packed else W), dtype=torch.uint8, device=pages.device)
+    _check(_lib.abin_binarize_batched(METHODS[method], _ptr(pages), pages.stride(0), _ptr(out), out.stride(0), P, H,
+                                      W, pages.stride(1), out.stride(1), MASK_BITS if packed else MASK_U8, h, w,
+                                      param0, param1, L, flags, _ptr(counters), _stream(stream)))
+    return out
+
+
+def binarize_band(method: str, held: torch.Tensor, row0: int, H_global: int, halo_top: int, halo_bot: int, h: int,
+                  w: int, param0: float, param1: float = 128.0, L: int = -1, packed: bool = False, out=None,
+                  flags: int = 0, counters: torch.Tensor = None, stream=None) -> torch.Tensor:
+    """Rows [row0, row0 + H_band) of an H_global-row image; `held` holds rows
+    [row0 - halo_top, row0 + H_band + halo_bot)."""
+    Hh, W, pitch = _img2d(held)
+    H_band = Hh - halo_top - halo_bot
+    out = _alloc_mask(H_band, W, packed, held.device) if out is None else out
+    _check(_lib.abin_binarize_band(METHODS[method], _ptr(held), H_band, W, pitch, row0, H_global, halo_top, halo_bot,
+                                   _ptr(out), out.stride(0), MASK_BITS if packed else MASK_U8, h, w, param0, param1, L,
+                                   flags, _ptr(counters), _stream(stream)))
+    return out
+
+
+def global_min(pages: torch.Tensor, stream=None) -> torch.Tensor:
+    """Per-page global minimum gray level L (Table 1 notation), on device."""
+    if pages.dim() == 2:
+        pages = pages.unsqueeze(0)
+    P, H, W = pages.shape
+    L = torch.empty(P, dtype=torch.uint8, device=pages.device)
+    _check(_lib.abin_global_min(_ptr(pages), pages.stride(0), P, H, W, pages.stride(1), _ptr(L), _stream(stream)))
+    return L
+
+
+def stats(method: str, img: torch.Tensor, h: int, w: int, param0: float, param1: float = 128.0, L: int = -1,
+          stream=None) -> dict:
+    """Per-pixel c, d (uint64), n (uint32), t (double; Q for quantile) and mask."""
+    H, W, pitch = _img2d(img)
+    dev = img.device
+    c = torch.empty((H, W), dtype=torch.int64, device=dev)
+    d = torch.empty((H, W), dtype=torch.int64, device=dev)
+    n = torch.empty((H, W), dtype=torch.int32, device=dev)
+    t = torch.empty((H, W), dtype=torch.float64, device=dev)
+    m = torch.empty((H, W), dtype=torch.uint8, device=dev)
+    quant = method == "quantile"
+    _check(_lib.abin_stats(METHODS[method], _ptr(img), H, W, pitch, h, w, param0, param1, L, None if quant else _ptr(c),
+                           None if quant else _ptr(d), None if quant else _ptr(n), _ptr(t), _ptr(m), _stream(stream)))
+    out = {"t": t, "mask": m}
+    if not quant:
+        out.update(c=c, d=d, n=n)
+    return out
+
+
+def strerror(status: int) -> str:
+    return _lib.abin_strerror(status).decode()
+
+
+def raw():
+    """The ctypes handle (for the C-ABI conformance tests)."""
+    return _lib

@@ -1,0 +1,235 @@
+"""GPU parity (-m gpu): the CUDA path (through the C ABI) against the CPU
+oracle, element by element on seeded inputs.
+
+Bars (BASELINE.json north_star): masks, window sums, counts and quantiles
+bit-exact; thresholds (fp64, identical expression order, no contraction)
+within 1e-12 relative -- in practice bit-identical, which is also checked;
+near-ties (|I - t| < 1e-9) counted.
+"""
+import zlib
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1905_13038_b200 as ab  # noqa: E402
+from paper_1905_13038_b200 import abin  # noqa: E402
+
+DEV = torch.device("cuda:0")
+T_RTOL = 1e-12
+
+
+def to_dev(I: np.ndarray, pitch: int = None) -> torch.Tensor:
+    """Copy a (H, W) page to the device; pitch=None: 16-byte padded pitch
+    (TMA path), pitch=W: tight rows (generic loader when W % 16 != 0)."""
+    H, W = I.shape
+    if pitch is None:
+        pitch = (W + 15) // 16 * 16
+    buf = torch.zeros((H, pitch), dtype=torch.uint8, device=DEV)
+    buf[:, :W] = torch.from_numpy(np.ascontiguousarray(I)).to(DEV)
+    return buf[:, :W]
+
+
+PARAMS = {"sauvola": (0.5, 128.0), "niblack": (-0.2, 128.0), "wolf": (0.5, 128.0)}
+
+
+def run(method, x, h, w, packed=False, flags=0, counters=None):
+    k, R = PARAMS[method]
+    if method == "sauvola":
+        return ab.sauvola(x, h, w, k, R, packed=packed, flags=flags, counters=counters)
+    if method == "niblack":
+        return ab.niblack(x, h, w, k, packed=packed, flags=flags, counters=counters)
+    return ab.wolf(x, h, w, k, R, packed=packed, flags=flags, counters=counters)
+
+
+def check_full(method, I, h, w, pitch=None, packed=False, stats=True):
+    k, R = PARAMS[method]
+    ref = oracle.binarize(method, I, h, w, k, R, stats=stats)
+    x = to_dev(I, pitch)
+    cnt = torch.zeros(2, dtype=torch.int64, device=DEV)
+    m = run(method, x, h, w, packed=packed, counters=cnt)
+    got = m.cpu().numpy()
+    want = ref["mask"] if stats else ref
+    if packed:
+        want = oracle.pack_bits(want)
+    assert np.array_equal(got, want), f"{method} mask mismatch {I.shape} h={h} w={w} packed={packed}: " \
+                                      f"{int((got != want).sum())} px"
+    if stats:
+        assert int(cnt[0]) == ref["near_tie"]
+        s = ab.stats(method, x, h, w, k, R)
+        assert np.array_equal(s["c"].cpu().numpy().astype(np.uint64), ref["c"])
+        assert np.array_equal(s["d"].cpu().numpy().astype(np.uint64), ref["d"])
+        assert np.array_equal(s["n"].cpu().numpy().astype(np.uint64), ref["n"])
+        t = s["t"].cpu().numpy()
+        rel = np.abs(t - ref["t"]) / np.maximum(np.abs(ref["t"]), 1e-300)
+        assert rel.max() <= T_RTOL
+        assert np.array_equal(t, ref["t"]), "thresholds are not bit-identical"
+        assert np.array_equal(s["mask"].cpu().numpy(), ref["mask"])
+
+
+# ------------------------------------------------------------------ config 1
+
+@pytest.mark.parametrize("packed", [False, True])
+def test_config1_full_page(packed):
+    I = synth.page(512, 512, synth.config_seed(1))
+    check_full("sauvola", I, 32, 32, packed=packed)
+
+
+# ------------------------------------------------------------------ SPEC grid
+
+SPEC_WINDOWS = [(1, 1), (2, 2), (3, 3), (2, 5), (5, 2), (31, 31), (64, 64), (100, 7)]
+SPEC_SHAPES = [(1, 1), (7, 9), (33, 20), (3, 200), (200, 3), (64, 64)]
+
+
+@pytest.mark.parametrize("method", ["sauvola", "niblack", "wolf"])
+@pytest.mark.parametrize("hw", SPEC_WINDOWS)
+def test_spec_grid(method, hw):
+    rng = np.random.default_rng(zlib.crc32(f"{method}{hw}".encode()))
+    for (H, W) in SPEC_SHAPES:
+        I = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+        for pitch in (None, W):
+            check_full(method, I, hw[0], hw[1], pitch=pitch, stats=(pitch is None))
+
+
+@pytest.mark.parametrize("packed", [False, True])
+@pytest.mark.parametrize("shape,hw", [((300, 2100), (61, 61)), ((1030, 333), (32, 17)), ((77, 1500), (101, 101)),
+                                      ((260, 900), (255, 255)), ((129, 3000), (15, 400))])
+def test_multi_tile_ragged(shape, hw, packed):
+    # several strips and row bands, ragged right/bottom tails, odd widths
+    I = synth.page(*shape, seed=synth.config_seed(7, shape[0]), stain=True)
+    for method in ("sauvola", "niblack"):
+        check_full(method, I, *hw, packed=packed, stats=not packed)
+
+
+def test_generic_loader_equals_tma_path():
+    I = synth.page(200, 1000, synth.config_seed(8))
+    a = run("sauvola", to_dev(I), 31, 31).cpu().numpy()
+    b = run("sauvola", to_dev(I, pitch=1000), 31, 31).cpu().numpy()     # 1000 % 16 != 0
+    buf = torch.zeros(200 * 1000 + 1, dtype=torch.uint8, device=DEV)    # misaligned base
+    xm = buf[1:].view(200, 1000)
+    xm.copy_(torch.from_numpy(I).to(DEV))
+    c = run("sauvola", xm, 31, 31).cpu().numpy()
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
+# ------------------------------------------------------------------ adversarial
+
+def test_low_contrast_niblack():
+    # 128 +- 2: Niblack thresholds land within ~1e-13 of pixel values
+    I = synth.low_contrast(97, 131, 5)
+    for hw in [(3, 3), (7, 5), (31, 31)]:
+        check_full("niblack", I, *hw)
+
+
+@pytest.mark.parametrize("g", [0, 1, 128, 255])
+def test_constant_images(g):
+    I = synth.constant(45, 70, g)
+    for method in ("sauvola", "niblack", "wolf"):
+        check_full(method, I, 9, 12)
+
+
+def test_one_by_one_and_huge_windows():
+    I = synth.uniform_random(50, 60, 6)
+    for method in ("sauvola", "niblack", "wolf"):
+        check_full(method, I, 1, 1)
+        check_full(method, I, 99, 119)        # whole-image window from every pixel
+        check_full(method, I, 500, 3)         # taller than the image
+
+
+def test_accumulator_bounds_all_255():
+    # h = w = 257 on an all-255 image
+    I = synth.constant(300, 300, 255)
+    check_full("sauvola", I, 257, 257)
+
+
+def test_even_and_odd_windows_asymmetry():
+    I = synth.page(120, 150, 17)
+    for hw in [(4, 4), (4, 5), (5, 4), (6, 9), (32, 32), (33, 33)]:
+        check_full("sauvola", I, *hw)
+
+
+# ------------------------------------------------------------------ stats / misc
+
+def test_wolf_global_min_on_device():
+    P = synth.pages(3, 64, 80, synth.config_seed(3), stain=True)
+    x = torch.from_numpy(P).to(DEV)
+    L = ab.global_min(x).cpu().numpy()
+    assert list(L) == [int(p.min()) for p in P]
+
+
+def test_forced_u64_square_sums_equal_u32():
+    I = synth.page(300, 400, 23)
+    x = to_dev(I)
+    a = ab.sauvola(x, 101, 101, 0.34, 128.0, packed=True).cpu().numpy()
+    b = ab.sauvola(x, 101, 101, 0.34, 128.0, packed=True, flags=abin.FORCE_U64_SQ).cpu().numpy()
+    assert np.array_equal(a, b)
+    assert np.array_equal(a, oracle.pack_bits(oracle.binarize("sauvola", I, 101, 101, 0.34, 128.0)))
+
+
+def test_batched_pages_equal_single_pages():
+    P = synth.pages(5, 130, 210, synth.config_seed(3), stain=True)
+    x = torch.from_numpy(P).to(DEV)
+    for method, (k, R) in PARAMS.items():
+        mb = ab.binarize_batched(method, x, 61, 61, k, R).cpu().numpy()
+        for p in range(5):
+            ref = oracle.binarize(method, P[p], 61, 61, k, R)
+            assert np.array_equal(mb[p], ref), (method, p)
+
+
+def test_band_decomposition_equals_whole_image():
+    # K7: G row bands with halo rows (o-1 above, u below) reproduce the
+    # whole-image mask bit for bit (single process, one GPU).
+    I = synth.page(1000, 700, 29)
+    Hg = I.shape[0]
+    for (h, w), method in [((101, 101), "sauvola"), ((32, 32), "niblack"), ((51, 51), "quantile")]:
+        k, R = PARAMS.get(method, (0.5, 128.0))
+        o, u = (h + 1) // 2, h // 2
+        if method == "quantile":
+            whole, _ = oracle.quantile(I, h, w, 0.5)
+        else:
+            whole = oracle.binarize(method, I, h, w, k, R)
+        for G in (2, 3, 8):
+            bounds = np.linspace(0, Hg, G + 1).astype(int)
+            parts = []
+            for g in range(G):
+                r0, r1 = bounds[g], bounds[g + 1]
+                top = min(o - 1, r0)
+                bot = min(u, Hg - r1)
+                held = to_dev(np.ascontiguousarray(I[r0 - top:r1 + bot]))
+                m = ab.binarize_band(method, held, r0, Hg, top, bot, h, w, 0.5 if method == "quantile" else k, R)
+                parts.append(m.cpu().numpy())
+            assert np.array_equal(np.concatenate(parts), whole), (method, G)
+
+
+# ------------------------------------------------------------------ quantile
+
+@pytest.mark.parametrize("q", [0.5, 0.1, 0.9, 1.0, 0.001])
+def test_quantile_small(q):
+    rng = np.random.default_rng(int(q * 1000))
+    for (H, W), (h, w) in [((33, 41), (5, 5)), ((64, 200), (51, 51)), ((7, 300), (4, 9)), ((100, 3), (3, 100))]:
+        I = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+        mref, Qref = oracle.quantile(I, h, w, q)
+        for pitch in (None, W):
+            x = to_dev(I, pitch)
+            m = ab.quantile(x, h, w, q).cpu().numpy()
+            assert np.array_equal(m, mref)
+            mb = ab.quantile(x, h, w, q, packed=True).cpu().numpy()
+            assert np.array_equal(mb, oracle.pack_bits(mref))
+        s = ab.stats("quantile", to_dev(I), h, w, q)
+        assert np.array_equal(s["t"].cpu().numpy(), Qref.astype(np.float64))
+
+
+def test_quantile_document_page():
+    I = synth.page(300, 500, synth.config_seed(5))
+    for q in (0.5, 0.1, 0.9):
+        mref, _ = oracle.quantile(I, 51, 51, q)
+        m = ab.quantile(to_dev(I), 51, 51, q).cpu().numpy()
+        assert np.array_equal(m, mref), q
