@@ -1,0 +1,391 @@
+"""bench.py -- the driver's benchmark contract for the abin hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 3]
+
+One step = one pass of the whole hot path (moments -> Sauvola threshold ->
+mask) over one batch of synthetic pages resident in HBM.  The default
+workload is BASELINE.json config 3 (the large-page config the >= 70 % roofline
+target is quoted on): 64 pages of 7016 x 4960 uint8 (A4 @ 600 dpi) with the
+stain blob, Sauvola k = 0.5, R = 128, h = w = 61, byte mask.  Pages are
+independent, so N GPUs each binarize their own 64-page batch (weak scaling,
+no data-path collective).  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (oracle/, the only other place bench.py
+executes it) on the host cores, on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402  (input generator: no method arithmetic)
+
+METRIC = "binarized gigapixels/s (Sauvola) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "Gpx/s"
+
+CONFIGS = {
+    # cfg: (pages, H, W, h, w, method, k, R, packed, stain, label)
+    1: (1, 512, 512, 32, 32, "sauvola", 0.5, 128.0, False, False,
+        "config1: 1 page 512x512 u8, Sauvola k=0.5 R=128 h=w=32, u8 mask"),
+    2: (1, 3300, 2550, 63, 63, "sauvola", 0.5, 128.0, False, False,
+        "config2: 1 page 3300x2550 u8 (letter @300dpi), Sauvola k=0.5 R=128 h=w=63, u8 mask"),
+    3: (64, 7016, 4960, 61, 61, "sauvola", 0.5, 128.0, False, True,
+        "config3: 64 pages x 7016x4960 u8 (A4 @600dpi) + stain, Sauvola k=0.5 R=128 h=w=61, u8 mask"),
+    4: (1, 32768, 32768, 101, 101, "sauvola", 0.34, 128.0, True, False,
+        "config4: 1 page 32768x32768 u8, Sauvola k=0.34 R=128 h=w=101, forced u64 square sums, bit mask"),
+    5: (1, 4096, 4096, 51, 51, "quantile", 0.5, 0.0, False, False,
+        "config5: 1 page 4096x4096 u8, local median (q=0.5) 51x51, u8 mask"),
+}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(cfg):
+    """dram read+write bytes per launch of the dominant kernel, from the
+    committed ncu --set full summary (None if not captured for this config)."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(path):
+        return None
+    d = json.load(open(path))
+    e = d.get(f"config{cfg}")
+    return None if e is None else e.get("dram_bytes_per_launch")
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """Samples SM clock and clock-event reasons with NVML during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, torch_dev):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            h = None
+            try:  # match the CUDA device to its NVML handle by UUID
+                import torch
+                want = str(torch.cuda.get_device_properties(torch_dev).uuid).lower()
+                for i in range(pynvml.nvmlDeviceGetCount()):
+                    hi = pynvml.nvmlDeviceGetHandleByIndex(i)
+                    u = pynvml.nvmlDeviceGetUUID(hi)
+                    u = (u.decode() if isinstance(u, bytes) else u).lower()
+                    if want and want in u:
+                        h = hi
+                        break
+            except Exception:
+                h = None
+            if h is None:
+                h = pynvml.nvmlDeviceGetHandleByIndex(torch_dev.index or 0)
+            self.h = h
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # NVML missing: report nothing rather than guess
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [k for k, v in self.REASONS.items() if self.reasons & v]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- distributed
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_pages(cfg, rank, scaling, world):
+    P, H, W, h, w, method, k, R, packed, stain, _ = CONFIGS[cfg]
+    if scaling == "strong" and P > 1:
+        P = (P + world - 1) // world
+        first = rank * P
+    else:
+        first = rank * P
+    pages = np.empty((P, H, W), np.uint8)
+    synth.pages(P, H, W, synth.config_seed(cfg, first), stain=stain, out=pages)
+    return pages
+
+
+def reference_main(args):
+    """--impl reference: the CPU oracle as it stands, rank 0 only."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    cfg = args.config
+    P, H, W, h, w, method, k, R, packed, stain, label = CONFIGS[cfg]
+    page = np.empty((H, W), np.uint8)
+    synth.page(H, W, synth.config_seed(cfg, 0), stain=stain, out=page)
+    cores = oracle.num_threads()
+    # bounded sample: a full-width band of rows of page 0, sized (from a
+    # calibration band) so the whole warm-up + timed run takes ~2 minutes
+    per_step = min(3.0, max(0.2, 120.0 / max(1, args.steps + args.warmup)))
+    rows = min(H, 4)
+    t0 = time.perf_counter()
+    _oracle_band(oracle, method, page, rows, h, w, k, R)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    rows = int(max(1, min(H, rows * per_step / dt)))
+    for _ in range(args.warmup):
+        _oracle_band(oracle, method, page, rows, h, w, k, R)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _oracle_band(oracle, method, page, rows, h, w, k, R)
+        times.append(time.perf_counter() - t0)
+    px = rows * W
+    tmean = sum(times) / len(times)
+    value = px / tmean / 1e9
+    sample = f"rows 0..{rows - 1} (full width {W}) of page 0 of {label}; {px} px per step"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tmean * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic",
+            "config": {"workload": label, "sample_rows": rows},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _oracle_band(oracle, method, page, rows, h, w, k, R):
+    """Oracle on output rows [0, rows) of `page` (full width): the oracle sees
+    the rows the windows need and the page's true height for n."""
+    H, W = page.shape
+    rr = np.repeat(np.arange(rows, dtype=np.int64), W)
+    cc = np.tile(np.arange(W, dtype=np.int64), rows)
+    if method == "quantile":
+        return oracle.quantile_points(page, h, w, k, rr, cc)
+    return oracle.binarize_points(method, page, h, w, k, R, -1, rr, cc)
+
+
+def cpu_baseline(cfg, budget_s=12.0):
+    """The oracle, as it stands, on a bounded sample of the workload."""
+    import oracle
+    P, H, W, h, w, method, k, R, packed, stain, label = CONFIGS[cfg]
+    page = np.empty((H, W), np.uint8)
+    synth.page(H, W, synth.config_seed(cfg, 0), stain=stain, out=page)
+    rows = min(H, 4)
+    t0 = time.perf_counter()
+    _oracle_band(oracle, method, page, rows, h, w, k, R)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    rows2 = int(max(1, min(H, rows * (budget_s * 0.8) / dt)))
+    t0 = time.perf_counter()
+    _oracle_band(oracle, method, page, rows2, h, w, k, R)
+    dt2 = time.perf_counter() - t0
+    px = rows2 * W
+    return {"value": px / dt2 / 1e9, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"direct definition on rows 0..{rows2 - 1} (full width) of page 0 of {label}: "
+                      f"{px} px in {dt2:.2f} s"}
+
+
+def ours_main(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if args.gpus != world and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_1905_13038_b200 as ab
+    from paper_1905_13038_b200 import abin
+
+    cfg = args.config
+    P0, H, W, h, w, method, k, R, packed, stain, label = CONFIGS[cfg]
+    pages_np = make_pages(cfg, rank, args.scaling, world)
+    P = pages_np.shape[0]
+    pitch = (W + 15) // 16 * 16   # 16-byte row pitch: the TMA staging path
+    xbuf = torch.zeros((P, H, pitch), dtype=torch.uint8, device=dev)
+    xbuf[:, :, :W] = torch.from_numpy(pages_np).to(dev)
+    x = xbuf[:, :, :W]
+    cols = (W + 7) // 8 if packed else W
+    out = torch.empty((P, H, cols), dtype=torch.uint8, device=dev)
+    flags = abin.FORCE_U64_SQ if cfg == 4 else 0
+    counters = torch.zeros(2, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if P == 1:
+            if method == "quantile":
+                ab.quantile(x[0], h, w, k, packed=packed, out=out[0])
+            else:
+                ab.sauvola(x[0], h, w, k, R, packed=packed, out=out[0], flags=flags, counters=counters)
+        else:
+            ab.binarize_batched(method, x, h, w, k, R, packed=packed, out=out, flags=flags, counters=counters)
+
+    launches_per_step = 1
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # --- timed region (device-timed with CUDA events on the launching stream)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+
+    px_rank = P * H * W
+    px_total = px_rank * world
+    value = px_total * args.steps / (max_ms / 1e3) / 1e9
+    ms_per_step = max_ms / args.steps
+
+    # --- roofline of the dominant (only) kernel: algorithmic bytes / launch time
+    bytes_per_px = 1.0 + (0.125 if packed else 1.0)
+    avg_kern_s = (sum(kern_ms) / len(kern_ms)) / 1e3
+    achieved = px_rank * bytes_per_px / avg_kern_s / 1e9
+    peak, peak_kind = measured_peaks()
+    traffic = ncu_traffic(cfg)
+
+    # --- e2e: the same metric through the C ABI with HOST buffers (pinned),
+    # H2D of the inputs and D2H of the masks inside the timed region.
+    e2e = None
+    if not args.no_e2e:
+        hin = torch.from_numpy(pages_np).pin_memory()
+        hout = torch.empty((P, H, cols), dtype=torch.uint8).pin_memory()
+        cs = torch.cuda.current_stream(dev)
+
+        def e2e_step():
+            rc = abin.raw().abin_binarize_batched(
+                abin.METHODS[method], abin.ctypes.c_void_p(hin.data_ptr()), hin.stride(0),
+                abin.ctypes.c_void_p(hout.data_ptr()), hout.stride(0), P, H, W, hin.stride(1), hout.stride(1),
+                abin.MASK_BITS if packed else abin.MASK_U8, h, w, k, R, -1, flags | abin.HOST_IO, None,
+                abin.ctypes.c_void_p(cs.cuda_stream))
+            if rc != 0:
+                raise abin.AbinError(rc)
+
+        e2e_steps = max(2, min(args.steps, 5))
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_ev.record(cs)
+        for _ in range(e2e_steps):
+            e2e_step()
+        b_ev.record(cs)
+        torch.cuda.synchronize()
+        et = torch.tensor([a_ev.elapsed_time(b_ev)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e_ms = float(et.item()) / e2e_steps
+        ok = torch.equal(hout, out.cpu())
+        e2e = {"value": px_total / (e2e_ms / 1e3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(hin.numel()),
+               "d2h_bytes_per_step": int(hout.numel()), "ms_per_step": e2e_ms, "steps": e2e_steps,
+               "matches_device_path": bool(ok)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
+            "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
+            "config": {"workload": label, "pages_per_rank": P, "H": H, "W": W, "h": h, "w": w, "method": method,
+                       "k": k, "R": R, "mask": "bits" if packed else "u8",
+                       "l2": f"inputs {P * H * W / 1e9:.2f} GB per rank > 126 MB L2 (no flush needed)"
+                             if P * H * W > 4 * 126e6 else "L2 flushed between steps"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_kind": peak_kind, "algorithmic_bytes_per_px": bytes_per_px,
+                         "kernel_ms": avg_kern_s * 1e3},
+            "clocks": clk.summary(),
+            "gpu_launches": launches_per_step * args.steps,
+            "near_ties": int(counters[0].item()),
+            "fallbacks": int(counters[1].item()),
+        }
+        if e2e is not None:
+            line["e2e"] = e2e
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        return reference_main(args)
+    return ours_main(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

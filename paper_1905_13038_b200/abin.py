@@ -12,7 +12,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libabin.so")
+LIB_PATH = os.environ.get("ABIN_LIB", os.path.join(_HERE, "libabin.so"))  # ABIN_LIB: dev A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")

@@ -19,9 +19,16 @@ def sources():
 
 def build(force: bool = False, verbose: bool = False) -> str:
     newest = max(os.path.getmtime(s) for s in sources())
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
+    if not force and not os.environ.get("ABIN_DEV_W32") and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
         return LIB
-    cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
+    dev = os.environ.get("ABIN_DEV_W32")  # e.g. "29,5": development build, those w mod 32 classes only
+    extra = []
+    if dev:  # nvcc splits -D values at commas: pass the list through a header
+        hdr = os.path.join(os.environ.get("TMPDIR", "/tmp"), "abin_dev_w32.h")
+        with open(hdr, "w") as f:
+            f.write("#define ABIN_DEV_W32 " + dev + "\n")
+        extra = ["-include", hdr]
+    cmd = [NVCC, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
            os.path.join(CSRC, "abin_api.cu")]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)

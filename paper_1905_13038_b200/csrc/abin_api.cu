@@ -9,10 +9,12 @@
 #include <cstring>
 #include <cstdlib>
 #include <mutex>
+#include <utility>
 
 #include "../../include/abin.h"
 #include "globalmin.cuh"
 #include "moments.cuh"
+#include "moments_wide.cuh"
 #include "quantile.cuh"
 
 using namespace abin;
@@ -72,23 +74,23 @@ Window effective_window(int32_t h, int32_t w, int64_t Hg, int64_t W) {
   return x;
 }
 
-constexpr int G = 8;
 // internal test hook: force the generic (non-TMA) loader
 constexpr uint32_t ABIN_NO_TMA_INTERNAL = 1u << 30;
 constexpr int64_t kMaxDim = (int64_t)1 << 30;
 
-int choose_nt(int32_t w_eff) {
-  const int kh = (((w_eff + 1 + G - 1) / G) + 1) & ~1;
+// ---- wide-window fallback (moments_wide.cuh): CTA strips of NT*8 columns
+int choose_nt_wide(int32_t w_eff) {
+  const int kh = (((w_eff + 1 + 8 - 1) / 8) + 1) & ~1;
   if (kh <= 64) return 128;
   if (kh <= 190) return 256;
-  return 0;  // unsupported by the strip kernel
+  return 0;
 }
 
 template <int NT, int PH, bool D64, bool STATS>
-int launch_moments_t(const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st) {
+int launch_wide_t(const CUtensorMap& map, const wide::MomParams& p, int64_t n_tiles, cudaStream_t st) {
   constexpr int R_ = (NT == 128) ? 8 : 4;
-  constexpr size_t smem = moments_smem_bytes<NT, G, R_, D64>();
-  auto kern = k_moments<NT, G, PH, R_, D64, STATS>;
+  constexpr size_t smem = wide::moments_smem_bytes<NT, 8, R_, D64>();
+  auto kern = wide::k_moments<NT, 8, PH, R_, D64, STATS>;
   static bool attr_set = false;  // benign race: the attribute value is idempotent
   if (!attr_set) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -100,18 +102,85 @@ int launch_moments_t(const CUtensorMap& map, const MomParams& p, int64_t n_tiles
 }
 
 template <bool D64, bool STATS>
-int launch_moments_nt(int nt, int ph, const CUtensorMap& map, const MomParams& p, int64_t n_tiles,
-                      cudaStream_t st) {
-#define ABIN_PH(NT_)                                                         \
-  switch (ph) {                                                              \
-    case 0: return launch_moments_t<NT_, 0, D64, STATS>(map, p, n_tiles, st); \
-    case 1: return launch_moments_t<NT_, 1, D64, STATS>(map, p, n_tiles, st); \
-    case 2: return launch_moments_t<NT_, 2, D64, STATS>(map, p, n_tiles, st); \
-    default: return launch_moments_t<NT_, 3, D64, STATS>(map, p, n_tiles, st); \
+int launch_wide(int nt, int ph, const CUtensorMap& map, const wide::MomParams& p, int64_t n_tiles,
+                cudaStream_t st) {
+#define ABIN_PH(NT_)                                                      \
+  switch (ph) {                                                           \
+    case 0: return launch_wide_t<NT_, 0, D64, STATS>(map, p, n_tiles, st); \
+    case 1: return launch_wide_t<NT_, 1, D64, STATS>(map, p, n_tiles, st); \
+    case 2: return launch_wide_t<NT_, 2, D64, STATS>(map, p, n_tiles, st); \
+    default: return launch_wide_t<NT_, 3, D64, STATS>(map, p, n_tiles, st); \
   }
   if (nt == 128) ABIN_PH(128)
   ABIN_PH(256)
 #undef ABIN_PH
+}
+
+// ---- the warp-strip kernel (moments.cuh), one instantiation per w mod 32
+template <int W32, bool D64>
+int launch_fast_t(const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st) {
+  constexpr size_t smem = moments_smem_bytes();
+  auto kern = k_moments<W32, D64>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    attr_set = true;
+  }
+  kern<<<(unsigned)n_tiles, kNT, smem, st>>>(map, p);
+  CK(cudaGetLastError());
+  return ABIN_OK;
+}
+
+template <bool D64, int... Ws>
+int launch_fast_w(int w32, const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st,
+                  std::integer_sequence<int, Ws...>) {
+  int rc = ABIN_EINVAL;
+  ((w32 == Ws ? (rc = launch_fast_t<Ws, D64>(map, p, n_tiles, st), true) : false) || ...);
+  return rc;
+}
+
+template <bool D64>
+int launch_fast(int w32, const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st) {
+#ifdef ABIN_DEV_W32  // development builds: one window class only (fast compile)
+  return launch_fast_w<D64>(w32, map, p, n_tiles, st, std::integer_sequence<int, ABIN_DEV_W32>{});
+#else
+  return launch_fast_w<D64>(w32, map, p, n_tiles, st, std::make_integer_sequence<int, 32>{});
+#endif
+}
+
+// Certified bounds of the fp32 stages (K2).  u = 2^-24; the
+// derivation bounds |t~ - t*| from the fp32 roundings of m, q, v, the
+// approximate square root (relative error eps_sqrt) and the threshold
+// expression, with m <= 255, s <= 128, q <= 255^2; eps64 bounds the
+// double-precision sequence's own error |t_fp64 - t*|.
+struct FilterConsts {
+  float fa, fb, delta1, delta2;
+};
+
+FilterConsts filter_consts(int method, double k, double R) {
+  const double u = std::ldexp(1.0, -24);
+  const double eps_sqrt = 8 * u;
+  const double eps64 = 1e-6;
+  const double qmax = 255.0 * 255.0;
+  const double rv = std::sqrt(16.2 * u * qmax);                     // sqrt of the stage-1 bound on |v~ - v|
+  const double ds1 = rv + eps_sqrt * (128.0 + rv);                  // stage 1: |s~ - s|
+  const double ds2 = (4 * u + eps_sqrt) * 128.0 * 1.01;             // stage 2: relative error x s_max
+  auto bound = [&](double ds) {
+    if (method == M_SAUVOLA) {
+      const double al = std::fabs(1.0 - k), be = std::fabs(k / R), G = al + be * (128.0 + ds);
+      return 255.0 * be * ds + 8.1 * u * 255.0 * G;
+    }
+    if (method == M_NIBLACK) return std::fabs(k) * ds + u * (8.0 * 255.0 + 4.0 * std::fabs(k) * 128.0);
+    return std::fabs(k) * 255.0 * ds / R + u * (8.0 * 255.0 + 12.0 * std::fabs(k) * 255.0);  // Wolf
+  };
+  FilterConsts f;
+  if (method == M_SAUVOLA) { f.fa = (float)(1.0 - k); f.fb = (float)(k / R); }
+  else if (method == M_NIBLACK) { f.fa = 0.0f; f.fb = (float)k; }
+  else { f.fa = (float)k; f.fb = (float)(1.0 / R); }
+  f.delta1 = (float)(1.25 * (bound(ds1) + eps64) + 1e-6);
+  f.delta2 = (float)(1.25 * (bound(ds2) + eps64) + 1e-6);
+  return f;
 }
 
 // Validation shared by every entry point.
@@ -152,103 +221,134 @@ struct MomCall {
   uint8_t* mask_out;
 };
 
-int run_moments(const MomCall& c) {
-  const Window win = effective_window(c.h, c.w, c.H_global, c.W);
-  const int nt = choose_nt(win.w);
-  if (nt == 0) return ABIN_ERANGE;
-  if ((uint64_t)win.h > 66051u) return ABIN_ERANGE;  // column D_j must fit uint32 (255^2 h < 2^32)
-  // TMA needs a 16-byte aligned base and strides; otherwise the kernel's
-  // generic loader stages the rows.
-  const bool tma_ok = !((reinterpret_cast<uintptr_t>(c.in) & 15u) || (c.in_pitch & 15) ||
-                        (c.n_pages > 1 && (c.in_page_stride & 15))) && !(c.flags & ABIN_NO_TMA_INTERNAL);
+// Row bands: pick the band count so that the tile count fills whole waves
+// of resident CTAs while keeping the h-row warm-up (pure vertical adds) short.
+void choose_bands(int64_t col_tiles, int64_t H_out, int32_t h, int resident, int32_t* B, int32_t* n_bands) {
+  double best = 1e30;
+  int64_t bestB = H_out;
+  for (int64_t nb = 1; nb <= std::max<int64_t>(1, H_out / 32); ++nb) {
+    const int64_t Bc = (H_out + nb - 1) / nb;
+    const int64_t tiles = col_tiles * ((H_out + Bc - 1) / Bc);
+    const int64_t waves = (tiles + resident - 1) / resident;
+    // cost ~ waves x (B rows + h/3 warm-up rows, warm-up rows are cheaper)
+    const double cost = (double)waves * (double)(Bc + h / 3.0);
+    if (cost < best * 0.999) { best = cost; bestB = Bc; }
+    if (tiles > 64 * resident) break;
+  }
+  *B = (int32_t)bestB;
+  *n_bands = (int32_t)((H_out + bestB - 1) / bestB);
+}
+
+int encode_map(const MomCall& c, int box_rows, bool tma_ok, CUtensorMap* map) {
+  memset(map, 0, sizeof(*map));
+  if (!tma_ok) return ABIN_OK;
   PFN_encodeTiled enc = get_encode();
-  if (tma_ok && !enc) {
+  if (!enc) {
     snprintf(g_last_cuda_error, sizeof(g_last_cuda_error), "cuTensorMapEncodeTiled unavailable");
     return ABIN_ECUDA;
   }
-  const int R_ = nt == 128 ? 8 : 4;
-  CUtensorMap map;
-  memset(&map, 0, sizeof(map));
-  if (tma_ok) {
   cuuint64_t dims[3] = {(cuuint64_t)c.W, (cuuint64_t)c.buf_rows, (cuuint64_t)c.n_pages};
   cuuint64_t strides[2] = {(cuuint64_t)c.in_pitch,
                            (cuuint64_t)(c.n_pages > 1 ? c.in_page_stride : c.in_pitch * c.buf_rows)};
-  cuuint32_t box[3] = {256, (cuuint32_t)R_, 1};
+  cuuint32_t box[3] = {256, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(c.in), dims, strides, box, estr,
+  CUresult cr = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(c.in), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) {
     snprintf(g_last_cuda_error, sizeof(g_last_cuda_error), "cuTensorMapEncodeTiled failed (%d)", (int)cr);
     return ABIN_ECUDA;
   }
-  }
-  MomParams p;
-  memset(&p, 0, sizeof(p));
-  p.use_tma = tma_ok ? 1 : 0;
-  p.in = c.in;
-  p.in_pitch = c.in_pitch;
-  p.in_page_stride = c.in_page_stride;
-  p.buf_rows = c.buf_rows;
-  p.W = c.W;
-  p.H_out = c.H_out;
-  p.row0 = c.row0;
-  p.H_global = c.H_global;
-  p.buf_row0 = c.buf_row0;
-  p.out = c.out;
-  p.out_pitch = c.out_pitch;
-  p.out_page_stride = c.out_page_stride;
-  p.h = win.h; p.w = win.w; p.l = win.l; p.r = win.r; p.o = win.o; p.u = win.u;
-  p.fmt = c.fmt;
-  // KH halo threads (>= ceil((w+1)/G), rounded up to even so that strip
-  // origins stay 16-byte aligned); the last 2 threads only feed the byte
-  // funnel of their neighbours and produce no output.
-  p.KH = ((win.w + 1 + G - 1) / G + 1) & ~1;
-  p.T = (nt - p.KH - 2) * G;
-  p.n_strips = (int32_t)((c.W + p.T - 1) / p.T);
-  // Row bands: enough tiles for several waves, long enough to amortise the
-  // h-row warm-up.
-  {
-    const int64_t tiles_cols = (int64_t)p.n_strips * c.n_pages;
-    int64_t B = 1024;
-    while (B > 64 && tiles_cols * ((c.H_out + B - 1) / B) < 148 * 6) B /= 2;
-    p.B = (int32_t)B;
-    p.n_bands = (int32_t)((c.H_out + B - 1) / B);
-  }
-  p.method = c.method;
-  p.force_fp64 = (c.flags & ABIN_FORCE_FP64) ? 1 : 0;
-  p.out_vec_ok = ((reinterpret_cast<uintptr_t>(c.out) | (uintptr_t)c.out_pitch |
-                   (uintptr_t)(c.n_pages > 1 ? c.out_page_stride : 0)) & 7u) == 0;
-  p.k = c.k;
-  p.R = c.R;
-  p.L_fixed = c.L_override;
-  p.counters = c.counters;
-  p.c_out = c.c_out; p.d_out = c.d_out; p.n_out = c.n_out; p.t_out = c.t_out; p.mask_out = c.mask_out;
+  return ABIN_OK;
+}
+
+int run_moments(const MomCall& c) {
+  const Window win = effective_window(c.h, c.w, c.H_global, c.W);
+  if ((uint64_t)win.h > 66051u) return ABIN_ERANGE;  // column D_j must fit uint32 (255^2 h < 2^32)
+  const int KH = (win.w + 1 + kG - 1) / kG;
+  const bool fast = KH <= 31;
+  const int nt_wide = fast ? 0 : choose_nt_wide(win.w);
+  if (!fast && nt_wide == 0) return ABIN_ERANGE;
+  // TMA needs a 16-byte aligned base and strides; otherwise the kernels'
+  // generic loader stages the rows.
+  const bool tma_ok = !((reinterpret_cast<uintptr_t>(c.in) & 15u) || (c.in_pitch & 15) ||
+                        (c.n_pages > 1 && (c.in_page_stride & 15))) && !(c.flags & ABIN_NO_TMA_INTERNAL);
+  CUtensorMap map;
+  int rc = encode_map(c, fast ? kR : (nt_wide == 128 ? 8 : 4), tma_ok, &map);
+  if (rc) return rc;
 
   unsigned int* Lw = nullptr;
-  uint8_t* L8 = nullptr;
+  const uint8_t* L8 = nullptr;
   if (c.method == M_WOLF && c.L_override < 0) {
     CK(cudaMallocAsync(&Lw, (size_t)c.n_pages * 4 + (size_t)c.n_pages, c.stream));
-    L8 = reinterpret_cast<uint8_t*>(Lw + c.n_pages);
+    uint8_t* l8 = reinterpret_cast<uint8_t*>(Lw + c.n_pages);
     k_fill_u32<<<(unsigned)((c.n_pages + 255) / 256), 256, 0, c.stream>>>(Lw, c.n_pages, 0xFFu);
     // pages are whole images here (band mode requires L_override)
     k_global_min<<<dim3(148, (unsigned)c.n_pages), 256, 0, c.stream>>>(c.in, c.in_page_stride, c.H_out, c.W,
                                                                          c.in_pitch, Lw);
-    k_narrow_u8<<<(unsigned)((c.n_pages + 255) / 256), 256, 0, c.stream>>>(Lw, L8, c.n_pages);
+    k_narrow_u8<<<(unsigned)((c.n_pages + 255) / 256), 256, 0, c.stream>>>(Lw, l8, c.n_pages);
     CK(cudaGetLastError());
-    p.L_page = L8;
+    L8 = l8;
   }
   const bool d64 = (c.flags & ABIN_FORCE_U64_SQ) || (uint64_t)win.h * (uint64_t)win.w * 65025u >= (1ull << 32);
   const int ph = ((-win.w) % 4 + 4) % 4;
-  const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * c.n_pages;
   const bool stats = c.c_out || c.d_out || c.n_out || c.t_out || c.mask_out;
-  int rc;
-  if (stats)
-    rc = d64 ? launch_moments_nt<true, true>(nt, ph, map, p, n_tiles, c.stream)
-             : launch_moments_nt<false, true>(nt, ph, map, p, n_tiles, c.stream);
-  else
-    rc = d64 ? launch_moments_nt<true, false>(nt, ph, map, p, n_tiles, c.stream)
-             : launch_moments_nt<false, false>(nt, ph, map, p, n_tiles, c.stream);
+
+  if (fast) {
+    MomParams p;
+    memset(&p, 0, sizeof(p));
+    p.use_tma = tma_ok ? 1 : 0;
+    p.in = c.in; p.in_pitch = c.in_pitch; p.in_page_stride = c.in_page_stride; p.buf_rows = c.buf_rows;
+    p.W = c.W; p.H_out = c.H_out; p.row0 = c.row0; p.H_global = c.H_global; p.buf_row0 = c.buf_row0;
+    p.out = c.out; p.out_pitch = c.out_pitch; p.out_page_stride = c.out_page_stride;
+    p.h = win.h; p.w = win.w; p.l = win.l; p.r = win.r; p.o = win.o; p.u = win.u;
+    p.fmt = c.fmt;
+    p.KH = KH;
+    p.Tw = kG * (32 - KH);
+    p.n_strips = (int32_t)((c.W + (int64_t)kCW * p.Tw - 1) / ((int64_t)kCW * p.Tw));
+    choose_bands((int64_t)p.n_strips * c.n_pages, c.H_out, win.h, 148 * 4, &p.B, &p.n_bands);
+    p.method = c.method;
+    p.force_fp64 = (c.flags & ABIN_FORCE_FP64) ? 1 : 0;
+    p.k = c.k; p.R = c.R;
+    p.L_page = L8; p.L_fixed = c.L_override;
+    const FilterConsts f = filter_consts(c.method, c.k, c.R);
+    p.fa = f.fa; p.fb = f.fb; p.delta1 = f.delta1; p.delta2 = f.delta2;
+    p.inv_h = 1.0f / (float)win.h;
+    p.counters = c.counters;
+    p.c_out = c.c_out; p.d_out = c.d_out; p.n_out = c.n_out; p.t_out = c.t_out; p.mask_out = c.mask_out;
+    const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * c.n_pages;
+    p.stats = stats ? 1 : 0;
+    const int w32 = win.w % 32;
+    rc = d64 ? launch_fast<true>(w32, map, p, n_tiles, c.stream) : launch_fast<false>(w32, map, p, n_tiles, c.stream);
+  } else {
+    wide::MomParams p;
+    memset(&p, 0, sizeof(p));
+    p.use_tma = tma_ok ? 1 : 0;
+    p.in = c.in; p.in_pitch = c.in_pitch; p.in_page_stride = c.in_page_stride; p.buf_rows = c.buf_rows;
+    p.W = c.W; p.H_out = c.H_out; p.row0 = c.row0; p.H_global = c.H_global; p.buf_row0 = c.buf_row0;
+    p.out = c.out; p.out_pitch = c.out_pitch; p.out_page_stride = c.out_page_stride;
+    p.h = win.h; p.w = win.w; p.l = win.l; p.r = win.r; p.o = win.o; p.u = win.u;
+    p.fmt = c.fmt;
+    p.KH = ((win.w + 1 + 8 - 1) / 8 + 1) & ~1;
+    p.T = (nt_wide - p.KH - 2) * 8;
+    p.n_strips = (int32_t)((c.W + p.T - 1) / p.T);
+    choose_bands((int64_t)p.n_strips * c.n_pages, c.H_out, win.h, 148 * 2, &p.B, &p.n_bands);
+    p.method = c.method;
+    p.force_fp64 = 1;
+    p.out_vec_ok = ((reinterpret_cast<uintptr_t>(c.out) | (uintptr_t)c.out_pitch |
+                     (uintptr_t)(c.n_pages > 1 ? c.out_page_stride : 0)) & 7u) == 0;
+    p.k = c.k; p.R = c.R;
+    p.L_page = L8; p.L_fixed = c.L_override;
+    p.counters = c.counters;
+    p.c_out = c.c_out; p.d_out = c.d_out; p.n_out = c.n_out; p.t_out = c.t_out; p.mask_out = c.mask_out;
+    const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * c.n_pages;
+    if (stats)
+      rc = d64 ? launch_wide<true, true>(nt_wide, ph, map, p, n_tiles, c.stream)
+               : launch_wide<false, true>(nt_wide, ph, map, p, n_tiles, c.stream);
+    else
+      rc = d64 ? launch_wide<true, false>(nt_wide, ph, map, p, n_tiles, c.stream)
+               : launch_wide<false, false>(nt_wide, ph, map, p, n_tiles, c.stream);
+  }
   if (Lw) {
     cudaError_t e = cudaFreeAsync(Lw, c.stream);
     if (rc == ABIN_OK && e != cudaSuccess) return cuda_fail(e);
@@ -309,6 +409,108 @@ int run_quantile(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int
   return ABIN_OK;
 }
 
+
+// ---- ABIN_HOST_IO: host buffers streamed through device staging ----------
+// Pages move in chunks through NSTR internal streams (H2D copy, kernel, D2H
+// copy per chunk; consecutive chunks overlap on different streams / copy
+// engines).  The caller's stream waits for all of it.
+struct HostIoStreams {
+  int device = -1;
+  cudaStream_t s[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t done[3] = {nullptr, nullptr, nullptr};
+};
+
+int get_host_io_streams(HostIoStreams** out) {
+  static std::mutex mu;
+  static HostIoStreams per_dev[64];
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return ABIN_EINVAL;
+  std::lock_guard<std::mutex> lock(mu);
+  HostIoStreams& h = per_dev[dev];
+  if (h.device < 0) {
+    for (int i = 0; i < 3; ++i) {
+      CK(cudaStreamCreateWithFlags(&h.s[i], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&h.done[i], cudaEventDisableTiming));
+    }
+    h.device = dev;
+  }
+  *out = &h;
+  return ABIN_OK;
+}
+
+int run_moments(const MomCall& c);
+int run_quantile(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64_t H_held, int64_t W,
+                 int64_t in_pitch, uint8_t* out, int64_t out_pitch, int64_t out_page_stride, int32_t fmt, int32_t h,
+                 int32_t w, double q, int64_t row0, int64_t H_out, int64_t H_global, int64_t buf_rows,
+                 int64_t buf_row0, cudaStream_t st, double* Q_out);
+
+int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8_t* out, int64_t out_page_stride,
+                int64_t P, int64_t H, int64_t W, int64_t in_pitch, int64_t out_pitch, int32_t fmt, int32_t h,
+                int32_t w, double p0, double p1, int32_t L, uint32_t flags, uint64_t* counters, cudaStream_t st) {
+  HostIoStreams* hs = nullptr;
+  int rc = get_host_io_streams(&hs);
+  if (rc) return rc;
+  const int64_t dpitch = (W + 15) / 16 * 16;
+  const int64_t orow = fmt == ABIN_MASK_U8 ? W : (W + 7) / 8;
+  const int64_t dopitch = (orow + 15) / 16 * 16;
+  const int64_t dpage = dpitch * H, dopage = dopitch * H;
+  int64_t pc = std::max<int64_t>(1, std::min<int64_t>(P, ((int64_t)128 << 20) / std::max<int64_t>(dpage, 1)));
+  const int nstr = (int)std::min<int64_t>(3, (P + pc - 1) / pc);
+  uint8_t* buf = nullptr;
+  const size_t per = (size_t)(pc * (dpage + dopage));
+  {
+    cudaError_t e = cudaMallocAsync(&buf, per * nstr, st);
+    if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? ABIN_ENOMEM : cuda_fail(e);
+  }
+  cudaEvent_t ready;
+  CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  CK(cudaEventRecord(ready, st));
+  for (int i = 0; i < nstr; ++i) CK(cudaStreamWaitEvent(hs->s[i], ready, 0));
+  const bool contiguous_in = P == 1 || in_page_stride == H * in_pitch;
+  const bool contiguous_out = P == 1 || out_page_stride == H * out_pitch;
+  for (int64_t c0 = 0, ci = 0; c0 < P && rc == ABIN_OK; c0 += pc, ++ci) {
+    const int64_t np = std::min(pc, P - c0);
+    cudaStream_t s = hs->s[ci % nstr];
+    uint8_t* din = buf + (ci % nstr) * per;
+    uint8_t* dout = din + pc * dpage;
+    if (contiguous_in) {
+      CK(cudaMemcpy2DAsync(din, dpitch, in + c0 * in_page_stride, in_pitch, W, np * H, cudaMemcpyHostToDevice, s));
+    } else {
+      for (int64_t q = 0; q < np; ++q)
+        CK(cudaMemcpy2DAsync(din + q * dpage, dpitch, in + (c0 + q) * in_page_stride, in_pitch, W, H,
+                             cudaMemcpyHostToDevice, s));
+    }
+    if (method == ABIN_QUANTILE) {
+      rc = run_quantile(din, dpage, np, H, W, dpitch, dout, dopitch, dopage, fmt, h, w, p0, 0, H, H, H, 0, s, nullptr);
+    } else {
+      MomCall m;
+      memset(&m, 0, sizeof(m));
+      m.method = method; m.in = din; m.in_page_stride = dpage; m.buf_rows = H; m.n_pages = np;
+      m.W = W; m.in_pitch = dpitch; m.H_out = H; m.H_global = H; m.out = dout; m.out_pitch = dopitch;
+      m.out_page_stride = dopage; m.fmt = fmt; m.h = h; m.w = w; m.k = p0; m.R = p1; m.L_override = L;
+      m.flags = flags & ~(uint32_t)ABIN_HOST_IO; m.counters = counters; m.stream = s;
+      rc = run_moments(m);
+    }
+    if (rc) break;
+    if (contiguous_out) {
+      CK(cudaMemcpy2DAsync(out + c0 * out_page_stride, out_pitch, dout, dopitch, orow, np * H,
+                           cudaMemcpyDeviceToHost, s));
+    } else {
+      for (int64_t q = 0; q < np; ++q)
+        CK(cudaMemcpy2DAsync(out + (c0 + q) * out_page_stride, out_pitch, dout + q * dopage, dopitch, orow, H,
+                             cudaMemcpyDeviceToHost, s));
+    }
+  }
+  for (int i = 0; i < nstr; ++i) {
+    CK(cudaEventRecord(hs->done[i], hs->s[i]));
+    CK(cudaStreamWaitEvent(st, hs->done[i], 0));
+  }
+  CK(cudaFreeAsync(buf, st));
+  CK(cudaEventDestroy(ready));
+  return rc;
+}
+
 }  // namespace
 
 // ============================================================== public ABI
@@ -330,8 +532,10 @@ int abin_binarize_batched(int32_t method, const uint8_t* in, int64_t in_page_str
   const int64_t in_span = (n_pages - 1) * in_page_stride + in_bytes;
   const int64_t out_span = (n_pages - 1) * out_page_stride + out_bytes;
   if (overlaps(in, (size_t)in_span, out, (size_t)out_span)) return ABIN_EALIAS;
-  if (flags & ABIN_HOST_IO) return ABIN_EINVAL;  // not implemented yet
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (flags & ABIN_HOST_IO)
+    return run_host_io(method, in, in_page_stride, out, out_page_stride, n_pages, H, W, in_pitch, out_pitch,
+                       mask_format, h, w, param0, param1, L_override, flags, counters, st);
   if (method == ABIN_QUANTILE)
     return run_quantile(in, in_page_stride, n_pages, H, W, in_pitch, out, out_pitch, out_page_stride, mask_format, h,
                         w, param0, 0, H, H, H, 0, st, nullptr);
@@ -504,7 +708,7 @@ int abin_stats(int32_t method, const uint8_t* in, int64_t H, int64_t W, int64_t 
 
 void abin_limits(abin_limits_t* out) {
   if (!out) return;
-  out->max_window_w = 190 * G - 1;
+  out->max_window_w = 190 * 8 - 1;
   out->max_window_h = 66051;
   out->max_dim = kMaxDim;
 }
