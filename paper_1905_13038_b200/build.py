@@ -1,15 +1,24 @@
-"""Build libabin.so (the CUDA kernels + C ABI) in-tree for sm_100a."""
+"""Build libabin.so (the CUDA kernels + C ABI) in-tree for sm_100a.
+
+The kernel template instantiations are spread over several translation units
+(csrc/moments_part.cu x 8, csrc/wide_part.cu x 2, csrc/abin_api.cu) that nvcc
+compiles in parallel into build/*.o; they are then linked into one shared
+library.
+"""
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libabin.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-              "-shared", "-Xptxas", "-warn-spills"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills"]
+N_PARTS = 8
 
 
 def sources():
@@ -17,19 +26,36 @@ def sources():
         os.path.join(ROOT, "include", "abin.h")]
 
 
+def units():
+    """(object name, source, extra flags) for every translation unit."""
+    u = [("abin_api.o", "abin_api.cu", [])]
+    u += [(f"moments_part{k}.o", "moments_part.cu", [f"-DABIN_PART={k}"]) for k in range(N_PARTS)]
+    u += [(f"wide_part{d}.o", "wide_part.cu", [f"-DABIN_WIDE_D64={d}"]) for d in (0, 1)]
+    return u
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    newest = max(os.path.getmtime(s) for s in sources())
-    if not force and not os.environ.get("ABIN_DEV_W32") and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
+    newest = max(os.path.getmtime(s) for s in sources() + [os.path.abspath(__file__)])
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
         return LIB
-    dev = os.environ.get("ABIN_DEV_W32")  # e.g. "29,5": development build, those w mod 32 classes only
-    extra = []
-    if dev:  # nvcc splits -D values at commas: pass the list through a header
-        hdr = os.path.join(os.environ.get("TMPDIR", "/tmp"), "abin_dev_w32.h")
-        with open(hdr, "w") as f:
-            f.write("#define ABIN_DEV_W32 " + dev + "\n")
-        extra = ["-include", hdr]
-    cmd = [NVCC, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
-           os.path.join(CSRC, "abin_api.cu")]
+    os.makedirs(OBJ, exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include")]
+
+    def compile_one(unit):
+        obj, src, extra = unit
+        cmd = [NVCC, *NVCC_FLAGS, *extra, *inc, "-c", "-o", os.path.join(OBJ, obj), os.path.join(CSRC, src)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src} {extra}:\n{r.stderr}")
+        if verbose and r.stderr.strip():
+            print(r.stderr, file=sys.stderr)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(units()), os.cpu_count() or 4))) as ex:
+        objs = list(ex.map(compile_one, units()))
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *[os.path.join(OBJ, o) for o in objs]]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
@@ -38,4 +64,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -13,8 +13,7 @@
 
 #include "../../include/abin.h"
 #include "globalmin.cuh"
-#include "moments.cuh"
-#include "moments_wide.cuh"
+#include "launch.cuh"
 #include "quantile.cuh"
 
 using namespace abin;
@@ -86,67 +85,26 @@ int choose_nt_wide(int32_t w_eff) {
   return 0;
 }
 
-template <int NT, int PH, bool D64, bool STATS>
-int launch_wide_t(const CUtensorMap& map, const wide::MomParams& p, int64_t n_tiles, cudaStream_t st) {
-  constexpr int R_ = (NT == 128) ? 8 : 4;
-  constexpr size_t smem = wide::moments_smem_bytes<NT, 8, R_, D64>();
-  auto kern = wide::k_moments<NT, 8, PH, R_, D64, STATS>;
-  static bool attr_set = false;  // benign race: the attribute value is idempotent
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
+int launch_fast_any(int w32, bool d64, const CUtensorMap& map, const MomParams& p, int64_t n, cudaStream_t st) {
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (w32 >> 2) {
+    case 0: e = launch_fast_part0(w32, d64, map, p, n, st); break;
+    case 1: e = launch_fast_part1(w32, d64, map, p, n, st); break;
+    case 2: e = launch_fast_part2(w32, d64, map, p, n, st); break;
+    case 3: e = launch_fast_part3(w32, d64, map, p, n, st); break;
+    case 4: e = launch_fast_part4(w32, d64, map, p, n, st); break;
+    case 5: e = launch_fast_part5(w32, d64, map, p, n, st); break;
+    case 6: e = launch_fast_part6(w32, d64, map, p, n, st); break;
+    case 7: e = launch_fast_part7(w32, d64, map, p, n, st); break;
   }
-  kern<<<(unsigned)n_tiles, NT, smem, st>>>(map, p);
-  CK(cudaGetLastError());
-  return ABIN_OK;
+  return e == cudaSuccess ? ABIN_OK : cuda_fail(e);
 }
 
-template <bool D64, bool STATS>
-int launch_wide(int nt, int ph, const CUtensorMap& map, const wide::MomParams& p, int64_t n_tiles,
-                cudaStream_t st) {
-#define ABIN_PH(NT_)                                                      \
-  switch (ph) {                                                           \
-    case 0: return launch_wide_t<NT_, 0, D64, STATS>(map, p, n_tiles, st); \
-    case 1: return launch_wide_t<NT_, 1, D64, STATS>(map, p, n_tiles, st); \
-    case 2: return launch_wide_t<NT_, 2, D64, STATS>(map, p, n_tiles, st); \
-    default: return launch_wide_t<NT_, 3, D64, STATS>(map, p, n_tiles, st); \
-  }
-  if (nt == 128) ABIN_PH(128)
-  ABIN_PH(256)
-#undef ABIN_PH
-}
-
-// ---- the warp-strip kernel (moments.cuh), one instantiation per w mod 32
-template <int W32, bool D64>
-int launch_fast_t(const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st) {
-  constexpr size_t smem = moments_smem_bytes();
-  auto kern = k_moments<W32, D64>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    attr_set = true;
-  }
-  kern<<<(unsigned)n_tiles, kNT, smem, st>>>(map, p);
-  CK(cudaGetLastError());
-  return ABIN_OK;
-}
-
-template <bool D64, int... Ws>
-int launch_fast_w(int w32, const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st,
-                  std::integer_sequence<int, Ws...>) {
-  int rc = ABIN_EINVAL;
-  ((w32 == Ws ? (rc = launch_fast_t<Ws, D64>(map, p, n_tiles, st), true) : false) || ...);
-  return rc;
-}
-
-template <bool D64>
-int launch_fast(int w32, const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st) {
-#ifdef ABIN_DEV_W32  // development builds: one window class only (fast compile)
-  return launch_fast_w<D64>(w32, map, p, n_tiles, st, std::integer_sequence<int, ABIN_DEV_W32>{});
-#else
-  return launch_fast_w<D64>(w32, map, p, n_tiles, st, std::make_integer_sequence<int, 32>{});
-#endif
+int launch_wide_any(bool d64, bool stats, int nt, int ph, const CUtensorMap& map, const wide::MomParams& p,
+                    int64_t n, cudaStream_t st) {
+  const cudaError_t e = d64 ? launch_wide_d64(d64, stats, nt, ph, map, p, n, st)
+                            : launch_wide_d32(d64, stats, nt, ph, map, p, n, st);
+  return e == cudaSuccess ? ABIN_OK : cuda_fail(e);
 }
 
 // Certified bounds of the fp32 stages (K2).  u = 2^-24; the
@@ -319,7 +277,7 @@ int run_moments(const MomCall& c) {
     const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * c.n_pages;
     p.stats = stats ? 1 : 0;
     const int w32 = win.w % 32;
-    rc = d64 ? launch_fast<true>(w32, map, p, n_tiles, c.stream) : launch_fast<false>(w32, map, p, n_tiles, c.stream);
+    rc = launch_fast_any(w32, d64, map, p, n_tiles, c.stream);
   } else {
     wide::MomParams p;
     memset(&p, 0, sizeof(p));
@@ -342,12 +300,7 @@ int run_moments(const MomCall& c) {
     p.counters = c.counters;
     p.c_out = c.c_out; p.d_out = c.d_out; p.n_out = c.n_out; p.t_out = c.t_out; p.mask_out = c.mask_out;
     const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * c.n_pages;
-    if (stats)
-      rc = d64 ? launch_wide<true, true>(nt_wide, ph, map, p, n_tiles, c.stream)
-               : launch_wide<false, true>(nt_wide, ph, map, p, n_tiles, c.stream);
-    else
-      rc = d64 ? launch_wide<true, false>(nt_wide, ph, map, p, n_tiles, c.stream)
-               : launch_wide<false, false>(nt_wide, ph, map, p, n_tiles, c.stream);
+    rc = launch_wide_any(d64, stats, nt_wide, ph, map, p, n_tiles, c.stream);
   }
   if (Lw) {
     cudaError_t e = cudaFreeAsync(Lw, c.stream);

@@ -1,0 +1,30 @@
+// launch.cuh -- launchers of the moments kernels, split over several
+// translation units (moments_part.cu, wide_part.cu) so the 100+ template
+// instantiations compile in parallel.  Each returns a cudaError_t.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "moments.cuh"
+#include "moments_wide.cuh"
+
+namespace abin {
+// warp-strip kernel, w mod 32 = w32 (moments.cuh)
+cudaError_t launch_fast(int w32, bool d64, const CUtensorMap& map, const MomParams& p, int64_t n_tiles,
+                        cudaStream_t st);
+// CTA-strip kernel for wide windows (moments_wide.cuh)
+cudaError_t launch_wide(bool d64, bool stats, int nt, int ph, const CUtensorMap& map, const wide::MomParams& p,
+                        int64_t n_tiles, cudaStream_t st);
+// per-part entry points (defined by moments_part.cu compiled with -DABIN_PART=k)
+#define ABIN_N_PARTS 8
+#define ABIN_DECL_PART(k)                                                                                 \
+  cudaError_t launch_fast_part##k(int w32, bool d64, const CUtensorMap& map, const MomParams& p, int64_t n, \
+                                  cudaStream_t st);
+ABIN_DECL_PART(0) ABIN_DECL_PART(1) ABIN_DECL_PART(2) ABIN_DECL_PART(3)
+ABIN_DECL_PART(4) ABIN_DECL_PART(5) ABIN_DECL_PART(6) ABIN_DECL_PART(7)
+cudaError_t launch_wide_d64(bool d64, bool stats, int nt, int ph, const CUtensorMap& map, const wide::MomParams& p,
+                            int64_t n_tiles, cudaStream_t st);
+cudaError_t launch_wide_d32(bool d64, bool stats, int nt, int ph, const CUtensorMap& map, const wide::MomParams& p,
+                            int64_t n_tiles, cudaStream_t st);
+}  // namespace abin

@@ -79,7 +79,7 @@ struct MomParams {
 // The canonical sequence: Alg. 1 l.121-122 then the Table-1 row written left
 // to right, each operation explicitly rounded (no FMA contraction), so the
 // result is the plain IEEE-double evaluation of the paper's formula.
-__device__ __noinline__ double threshold_fp64(int method, uint64_t c, uint64_t d, uint32_t n, double k, double R,
+static __device__ __noinline__ double threshold_fp64(int method, uint64_t c, uint64_t d, uint32_t n, double k, double R,
                                               double L) {
   const double nd = (double)n;
   const double m = __ddiv_rn((double)c, nd);
@@ -131,6 +131,14 @@ __device__ __forceinline__ uint32_t byte_of(const uint4& v, int t) {
 
 constexpr int kG = 16;        // columns per lane
 
+// Bank-conflict-free layout of a warp's published 512-column row (C, D and
+// the -1/ncol table): column s lives at word
+//   ((s/4) mod 4) * 128 + (s/16) * 4 + s mod 4,
+// i.e. [4-column chunk g][lane][4], so a warp-wide 16-byte access to chunk g
+// of 32 consecutive lanes (publish) or of 32 lanes offset by a common column
+// shift (the leaving reads) touches 512 consecutive bytes.
+__device__ __forceinline__ int swz(int s) { return (((s >> 2) & 3) << 7) | ((s >> 4) << 2) | (s & 3); }
+
 __device__ __forceinline__ float ninv_sel(const float (&a)[16], int t) {
   float r = 0.0f;
 #pragma unroll
@@ -171,12 +179,12 @@ __device__ __forceinline__ void load_leaving(const uint32_t* cs, const uint32_t*
 // bits by prmt) and returns min |en|.
 template <int METHOD, int PH, typename DT>
 __device__ __forceinline__ float row_stage1(const uint32_t (&C)[16], const uint32_t (&D)[16], const uint32_t* cs,
-                                            const uint32_t* ds, uint32_t cc, DT dd, const float* nic,
-                                            float inv_nrow, const uint4& xc, float2 fa2, float2 fb2, float Lf,
-                                            uint32_t (&wv)[4]) {
+                                            const uint32_t* ds, const int (&lofs)[5], uint32_t cc, DT dd,
+                                            const float* nic, float inv_nrow, const uint4& xc, float2 fa2,
+                                            float2 fb2, float Lf, uint32_t (&wv)[4]) {
   const float2 nr2 = make_float2(inv_nrow, inv_nrow);
   float emin = __int_as_float(0x7f800000);
-  uint4 qc = *reinterpret_cast<const uint4*>(cs), qd = *reinterpret_cast<const uint4*>(ds);
+  uint4 qc = *reinterpret_cast<const uint4*>(cs + lofs[0]), qd = *reinterpret_cast<const uint4*>(ds + lofs[0]);
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
     // leaving values of outputs 4g .. 4g+3 = words PH .. PH+3 of (qc, next)
@@ -185,12 +193,12 @@ __device__ __forceinline__ float row_stage1(const uint32_t (&C)[16], const uint3
       cl[0] = qc.x; cl[1] = qc.y; cl[2] = qc.z; cl[3] = qc.w;
       dl[0] = qd.x; dl[1] = qd.y; dl[2] = qd.z; dl[3] = qd.w;
       if (g < 3) {
-        qc = *reinterpret_cast<const uint4*>(cs + 4 * g + 4);
-        qd = *reinterpret_cast<const uint4*>(ds + 4 * g + 4);
+        qc = *reinterpret_cast<const uint4*>(cs + lofs[g + 1]);
+        qd = *reinterpret_cast<const uint4*>(ds + lofs[g + 1]);
       }
     } else {
-      const uint4 nc = *reinterpret_cast<const uint4*>(cs + 4 * g + 4);
-      const uint4 nd = *reinterpret_cast<const uint4*>(ds + 4 * g + 4);
+      const uint4 nc = *reinterpret_cast<const uint4*>(cs + lofs[g + 1]);
+      const uint4 nd = *reinterpret_cast<const uint4*>(ds + lofs[g + 1]);
       const uint32_t c8[8] = {qc.x, qc.y, qc.z, qc.w, nc.x, nc.y, nc.z, nc.w};
       const uint32_t d8[8] = {qd.x, qd.y, qd.z, qd.w, nd.x, nd.y, nd.z, nd.w};
 #pragma unroll
@@ -198,7 +206,7 @@ __device__ __forceinline__ float row_stage1(const uint32_t (&C)[16], const uint3
       qc = nc;
       qd = nd;
     }
-    const float4 ni4 = *reinterpret_cast<const float4*>(nic + 4 * g);
+    const float4 ni4 = *reinterpret_cast<const float4*>(nic + 128 * g);
     const float nis[4] = {ni4.x, ni4.y, ni4.z, ni4.w};
     const uint32_t wd = g == 0 ? xc.x : (g == 1 ? xc.y : (g == 2 ? xc.z : xc.w));
     float e4[4];
@@ -431,6 +439,9 @@ __global__ void __launch_bounds__(kNT, 4) k_moments(const __grid_constant__ CUte
   uint32_t* cb = pub + warp * (2 * kWarpRow);         // this warp's published C row
   uint32_t* db = cb + kWarpRow;                       //                      D row
   const int st0 = valid_lane ? (kG * lane - p.w - PH) : 0;  // 4-aligned start of the leaving reads
+  int lofs[5];                                        // swizzled word offsets of the leaving chunks
+#pragma unroll
+  for (int g = 0; g < 5; ++g) lofs[g] = swz(min(st0 + 4 * g, kWarpRow - 4));
   const float Lf = (p.method == M_WOLF) ? (float)(p.L_fixed >= 0 ? p.L_fixed : (int)p.L_page[page]) : 0.0f;
   const bool slow_all = p.stats || p.force_fp64;
   const int method = p.method;
@@ -438,12 +449,13 @@ __global__ void __launch_bounds__(kNT, 4) k_moments(const __grid_constant__ CUte
 
   // negated reciprocals of the clamped column counts (n = ncol * nrow,
   // PAPER.md:118), kept in shared memory (read back as float4 per 4 outputs)
-  float* nic = nic_all + warp * kWarpRow + kG * lane;
+  float* nicw = nic_all + warp * kWarpRow;
+  const float* nic = nicw + 4 * lane;               // chunk g of this lane at nic + 128 g
 #pragma unroll
   for (int t = 0; t < kG; ++t) {
     const int64_t j = j0 + t;
     const int64_t nc = max((int64_t)1, min(j + p.r, p.W - 1) - max(j - p.l, (int64_t)-1));
-    nic[t] = -__frcp_rn((float)nc);
+    nicw[swz(kG * lane + t)] = -__frcp_rn((float)nc);
   }
   __syncwarp();
   const float2 fa2 = make_float2(p.fa, p.fa), fb2 = make_float2(p.fb, p.fb);
@@ -512,8 +524,8 @@ __global__ void __launch_bounds__(kNT, 4) k_moments(const __grid_constant__ CUte
       __syncwarp();
 #pragma unroll
       for (int t = 0; t < kG; t += 4) {
-        *reinterpret_cast<uint4*>(cb + kG * lane + t) = make_uint4(C[t], C[t + 1], C[t + 2], C[t + 3]);
-        *reinterpret_cast<uint4*>(db + kG * lane + t) = make_uint4(D[t], D[t + 1], D[t + 2], D[t + 3]);
+        *reinterpret_cast<uint4*>(cb + 32 * t + 4 * lane) = make_uint4(C[t], C[t + 1], C[t + 2], C[t + 3]);
+        *reinterpret_cast<uint4*>(db + 32 * t + 4 * lane) = make_uint4(D[t], D[t + 1], D[t + 2], D[t + 3]);
       }
       // lane totals (pairwise) and the partial prefix up to position PP
       uint32_t partc = 0;
@@ -561,13 +573,13 @@ __global__ void __launch_bounds__(kNT, 4) k_moments(const __grid_constant__ CUte
       float emin;
       switch (method) {  // warp-uniform
         case M_SAUVOLA:
-          emin = row_stage1<M_SAUVOLA, PH>(C, D, cb + st0, db + st0, c0, d0, nic, inv_nrow, xc, fa2, fb2, Lf, wv);
+          emin = row_stage1<M_SAUVOLA, PH>(C, D, cb, db, lofs, c0, d0, nic, inv_nrow, xc, fa2, fb2, Lf, wv);
           break;
         case M_NIBLACK:
-          emin = row_stage1<M_NIBLACK, PH>(C, D, cb + st0, db + st0, c0, d0, nic, inv_nrow, xc, fa2, fb2, Lf, wv);
+          emin = row_stage1<M_NIBLACK, PH>(C, D, cb, db, lofs, c0, d0, nic, inv_nrow, xc, fa2, fb2, Lf, wv);
           break;
         default:
-          emin = row_stage1<M_WOLF, PH>(C, D, cb + st0, db + st0, c0, d0, nic, inv_nrow, xc, fa2, fb2, Lf, wv);
+          emin = row_stage1<M_WOLF, PH>(C, D, cb, db, lofs, c0, d0, nic, inv_nrow, xc, fa2, fb2, Lf, wv);
           break;
       }
       uint32_t ambits = slow_all ? vmask : 0u;
@@ -585,8 +597,8 @@ __global__ void __launch_bounds__(kNT, 4) k_moments(const __grid_constant__ CUte
 #pragma unroll
           for (int z = 0; z < kG; ++z)
             if (z == t) { Ct = C[z]; Dt = D[z]; }
-          cc += Ct - cb[st0 + PH + t];
-          dd += (DT)Dt - (DT)db[st0 + PH + t];
+          cc += Ct - cb[swz(st0 + PH + t)];
+          dd += (DT)Dt - (DT)db[swz(st0 + PH + t)];
           if (!((ambits >> t) & 1u)) continue;
           const int64_t j = j0 + t;
           const uint32_t n =
@@ -597,7 +609,7 @@ __global__ void __launch_bounds__(kNT, 4) k_moments(const __grid_constant__ CUte
           uint32_t mk = 0;
           if (!slow_all) {
             // stage 1 again for this pixel (is it really ambiguous?)
-            const float ninv = nic[t] * inv_nrow;
+            const float ninv = nicw[swz(kG * lane + t)] * inv_nrow;
             const float mn = (float)cc * ninv, qn = (float)dd * ninv;
             const float s1 = sqrt_approx(fabsf(__fmaf_rn(mn, mn, qn)));
             const float e1 = (float)I - threshold_f32(p.method, -mn, s1, p.fa, p.fb, Lf);

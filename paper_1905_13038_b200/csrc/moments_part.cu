@@ -1,0 +1,41 @@
+// moments_part.cu -- instantiations of the warp-strip moments kernel for
+// w mod 32 in [4 ABIN_PART, 4 ABIN_PART + 4), both square-sum widths.
+// Compiled ABIN_N_PARTS times (build.py) with -DABIN_PART=0..7.
+#include "launch.cuh"
+
+#ifndef ABIN_PART
+#error "compile with -DABIN_PART=k"
+#endif
+#define ABIN_CAT2(a, b) a##b
+#define ABIN_CAT(a, b) ABIN_CAT2(a, b)
+
+namespace abin {
+namespace {
+template <int W32, bool D64>
+cudaError_t launch_one(const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st) {
+  constexpr size_t smem = moments_smem_bytes();
+  auto kern = k_moments<W32, D64>;
+  static bool attr_set = false;  // benign race: the attribute values are idempotent
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  kern<<<(unsigned)n_tiles, kNT, smem, st>>>(map, p);
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t ABIN_CAT(launch_fast_part, ABIN_PART)(int w32, bool d64, const CUtensorMap& map, const MomParams& p,
+                                                  int64_t n, cudaStream_t st) {
+  constexpr int b = 4 * ABIN_PART;
+  switch (w32 - b) {
+    case 0: return d64 ? launch_one<b + 0, true>(map, p, n, st) : launch_one<b + 0, false>(map, p, n, st);
+    case 1: return d64 ? launch_one<b + 1, true>(map, p, n, st) : launch_one<b + 1, false>(map, p, n, st);
+    case 2: return d64 ? launch_one<b + 2, true>(map, p, n, st) : launch_one<b + 2, false>(map, p, n, st);
+    case 3: return d64 ? launch_one<b + 3, true>(map, p, n, st) : launch_one<b + 3, false>(map, p, n, st);
+  }
+  return cudaErrorInvalidValue;
+}
+}  // namespace abin
