@@ -5,7 +5,7 @@
 # into gpurun_out/ and drops the .ncu-rep.
 tag=$1; shift
 "$@" > gpurun_out/${tag}_plain.log 2>&1 || { echo "plain run failed"; exit 1; }
-ncu --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-k_moments} -c 1 -o /tmp/${tag} "$@" > gpurun_out/${tag}_ncu.log 2>&1
+ncu -f --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-k_moments} -c 1 -o /tmp/${tag} "$@" > gpurun_out/${tag}_ncu.log 2>&1
 ncu -i /tmp/${tag}.ncu-rep --page raw --csv > gpurun_out/${tag}_raw.csv 2>/dev/null
 ncu -i /tmp/${tag}.ncu-rep --page details --csv > gpurun_out/${tag}_details.csv 2>/dev/null
 ncu -i /tmp/${tag}.ncu-rep --page source --csv --print-source sass > gpurun_out/${tag}_sass.csv 2>/dev/null
