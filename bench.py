@@ -54,15 +54,18 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-def ncu_traffic(cfg):
+def ncu_traffic(cfg, px_per_launch):
     """dram read+write bytes per launch of the dominant kernel, from the
-    committed ncu --set full summary (None if not captured for this config)."""
+    committed `ncu --set full` summary (profiles/ncu_summary.json, written by
+    tools/summarize_profile.py); None unless it was captured on this config
+    with the same launch size."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(path):
         return None
-    d = json.load(open(path))
-    e = d.get(f"config{cfg}")
-    return None if e is None else e.get("dram_bytes_per_launch")
+    e = json.load(open(path)).get(f"config{cfg}")
+    if e is None or int(e.get("px_per_launch", -1)) != int(px_per_launch):
+        return None
+    return e.get("dram_bytes_per_launch")
 
 
 # ---------------------------------------------------------------- clocks
@@ -301,7 +304,7 @@ def ours_main(args):
     avg_kern_s = (sum(kern_ms) / len(kern_ms)) / 1e3
     achieved = px_rank * bytes_per_px / avg_kern_s / 1e9
     peak, peak_kind = measured_peaks()
-    traffic = ncu_traffic(cfg)
+    traffic = ncu_traffic(cfg, px_rank)
 
     # --- e2e: the same metric through the C ABI with HOST buffers (pinned),
     # H2D of the inputs and D2H of the masks inside the timed region.
