@@ -233,3 +233,28 @@ def test_quantile_document_page():
         mref, _ = oracle.quantile(I, 51, 51, q)
         m = ab.quantile(to_dev(I), 51, 51, q).cpu().numpy()
         assert np.array_equal(m, mref), q
+
+
+# ------------------------------------------------------------ multi-GPU driver
+
+@pytest.mark.parametrize("G,h,w,packed", [(4, 101, 101, True), (3, 32, 31, False), (2, 9, 8, False)])
+def test_driver_bands_emulated_on_one_gpu(G, h, w, packed):
+    """paper_1905_13038_b200.dist.run_band on G emulated ranks (halos filled
+    from the global image instead of NCCL): interior / top / bottom strips
+    launched as on the real multi-GPU path; the concatenated masks equal the
+    oracle's whole-image mask."""
+    from paper_1905_13038_b200 import dist as adist
+    H, W = 403, 700
+    I = synth.page(H, W, synth.config_seed(4, 3))
+    k = 0.34
+    parts = []
+    for g in range(G):
+        band = adist.make_band(H, W, h, g, G, device=DEV)
+        band.buf.copy_(torch.from_numpy(I[band.r0 - band.top:band.r1 + band.bot]).to(DEV))
+        parts.append(adist.run_band("sauvola", band, h, w, k, 128.0, packed=packed, rank=g, world=G,
+                                    exchange=False, flags=abin.FORCE_U64_SQ).cpu().numpy())
+    got = np.concatenate(parts, axis=0)
+    want = oracle.binarize("sauvola", I, h, w, k, 128.0)
+    if packed:
+        want = oracle.pack_bits(want)
+    assert np.array_equal(got, want)
