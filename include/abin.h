@@ -33,6 +33,10 @@
  * -------------------------------------
  * - Images are uint8, row-major, `H` rows of `W` pixels, rows `pitch` bytes
  *   apart (pitch >= W).  Page batches place page p at `in + p*in_page_stride`.
+ *   When the base, pitch and page stride are multiples of 16 bytes the rows are
+ *   staged by TMA in whole 16-byte chunks: the bytes of a row's last partial
+ *   chunk (columns W .. ceil(W/16)*16 - 1, inside the pitch) must be readable;
+ *   their values are ignored.
  * - All image / mask pointers are DEVICE pointers (cudaMalloc'd or torch CUDA
  *   tensors) unless the flag ABIN_HOST_IO is given (abin_*_batched only): then
  *   `in` and `out` are HOST pointers (pinned memory recommended) and the
@@ -83,7 +87,9 @@ enum { ABIN_MASK_U8 = 0, ABIN_MASK_BITS = 1 };
 enum {
   ABIN_FORCE_U64_SQ = 1u << 0, /* accumulate window square sums d in uint64 even when uint32 is exact */
   ABIN_FORCE_FP64 = 1u << 1,   /* skip the fp32 filter: every pixel takes the exact fp64 sequence */
-  ABIN_HOST_IO = 1u << 2       /* (batched calls) in/out are host pointers; copies are part of the call */
+  ABIN_HOST_IO = 1u << 2,      /* (batched calls) in/out are host pointers; copies are part of the call */
+  ABIN_COUNT_STAGES = 1u << 3  /* `counters` has 3 entries; counters[2] += pixels the fp32 filter re-examined
+                                  from the exact integers (stage 2) */
 };
 
 /* ---- Sauvola (Table 1) --------------------------------------

@@ -28,7 +28,8 @@ _D = ctypes.c_double
 SAUVOLA, NIBLACK, WOLF, QUANTILE = 0, 1, 2, 3
 METHODS = {"sauvola": SAUVOLA, "niblack": NIBLACK, "wolf": WOLF, "quantile": QUANTILE}
 MASK_U8, MASK_BITS = 0, 1
-FORCE_U64_SQ, FORCE_FP64, HOST_IO = 1, 2, 4
+FORCE_U64_SQ, FORCE_FP64, HOST_IO, COUNT_STAGES = 1, 2, 4, 8
+V3_INTERNAL = 1 << 29  # internal test hook: the 4-warp-CTA kernel instead of the warp-CTA kernel
 OK, EINVAL, EALIAS, ERANGE, ECUDA, ENOMEM = 0, 1, 2, 3, 4, 5
 
 _lib.abin_sauvola.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _D, _D, _U32, _P, _P]

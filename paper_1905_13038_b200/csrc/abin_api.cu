@@ -75,6 +75,8 @@ Window effective_window(int32_t h, int32_t w, int64_t Hg, int64_t W) {
 
 // internal test hook: force the generic (non-TMA) loader
 constexpr uint32_t ABIN_NO_TMA_INTERNAL = 1u << 30;
+// internal test hook: the 4-warp-CTA kernel (moments.cuh) instead of the warp-CTA kernel (moments4.cuh)
+constexpr uint32_t ABIN_V3_INTERNAL = 1u << 29;
 constexpr int64_t kMaxDim = (int64_t)1 << 30;
 
 // ---- wide-window fallback (moments_wide.cuh): CTA strips of NT*8 columns
@@ -96,6 +98,21 @@ int launch_fast_any(int w32, bool d64, const CUtensorMap& map, const MomParams& 
     case 5: e = launch_fast_part5(w32, d64, map, p, n, st); break;
     case 6: e = launch_fast_part6(w32, d64, map, p, n, st); break;
     case 7: e = launch_fast_part7(w32, d64, map, p, n, st); break;
+  }
+  return e == cudaSuccess ? ABIN_OK : cuda_fail(e);
+}
+
+int launch_v4_any(int w32, bool d64, const CUtensorMap& map, const MomParams& p, int64_t n, cudaStream_t st) {
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (w32 >> 2) {
+    case 0: e = launch_v4_part0(w32, d64, map, p, n, st); break;
+    case 1: e = launch_v4_part1(w32, d64, map, p, n, st); break;
+    case 2: e = launch_v4_part2(w32, d64, map, p, n, st); break;
+    case 3: e = launch_v4_part3(w32, d64, map, p, n, st); break;
+    case 4: e = launch_v4_part4(w32, d64, map, p, n, st); break;
+    case 5: e = launch_v4_part5(w32, d64, map, p, n, st); break;
+    case 6: e = launch_v4_part6(w32, d64, map, p, n, st); break;
+    case 7: e = launch_v4_part7(w32, d64, map, p, n, st); break;
   }
   return e == cudaSuccess ? ABIN_OK : cuda_fail(e);
 }
@@ -220,6 +237,31 @@ int encode_map(const MomCall& c, int box_rows, bool tma_ok, CUtensorMap* map) {
   return ABIN_OK;
 }
 
+// v4 view of the pages: {16 bytes, ceil(W/16) chunks, rows, pages}; a box is
+// `chunks` whole chunks x `rows` rows (moments4.cuh).  Needs 16-byte aligned
+// base, pitch and page stride.
+int encode_map_chunks(const MomCall& c, int chunks, int rows, CUtensorMap* map) {
+  memset(map, 0, sizeof(*map));
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) {
+    snprintf(g_last_cuda_error, sizeof(g_last_cuda_error), "cuTensorMapEncodeTiled unavailable");
+    return ABIN_ECUDA;
+  }
+  cuuint64_t dims[4] = {16, (cuuint64_t)((c.W + 15) / 16), (cuuint64_t)c.buf_rows, (cuuint64_t)c.n_pages};
+  cuuint64_t strides[3] = {16, (cuuint64_t)c.in_pitch,
+                           (cuuint64_t)(c.n_pages > 1 ? c.in_page_stride : c.in_pitch * c.buf_rows)};
+  cuuint32_t box[4] = {16, (cuuint32_t)chunks, (cuuint32_t)rows, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult cr = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(c.in), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) {
+    snprintf(g_last_cuda_error, sizeof(g_last_cuda_error), "cuTensorMapEncodeTiled (chunks) failed (%d)", (int)cr);
+    return ABIN_ECUDA;
+  }
+  return ABIN_OK;
+}
+
 int run_moments(const MomCall& c) {
   const Window win = effective_window(c.h, c.w, c.H_global, c.W);
   if ((uint64_t)win.h > 66051u) return ABIN_ERANGE;  // column D_j must fit uint32 (255^2 h < 2^32)
@@ -231,8 +273,10 @@ int run_moments(const MomCall& c) {
   // generic loader stages the rows.
   const bool tma_ok = !((reinterpret_cast<uintptr_t>(c.in) & 15u) || (c.in_pitch & 15) ||
                         (c.n_pages > 1 && (c.in_page_stride & 15))) && !(c.flags & ABIN_NO_TMA_INTERNAL);
+  const bool use_v4 = fast && tma_ok && !(c.flags & ABIN_V3_INTERNAL);
   CUtensorMap map;
-  int rc = encode_map(c, fast ? kR : (nt_wide == 128 ? 8 : 4), tma_ok, &map);
+  int rc = use_v4 ? encode_map_chunks(c, v4::kChunks, v4::kR, &map)
+                  : encode_map(c, fast ? kR : (nt_wide == 128 ? 8 : 4), tma_ok, &map);
   if (rc) return rc;
 
   unsigned int* Lw = nullptr;
@@ -273,11 +317,28 @@ int run_moments(const MomCall& c) {
     p.fa = f.fa; p.fb = f.fb; p.delta1 = f.delta1; p.delta2 = f.delta2;
     p.inv_h = 1.0f / (float)win.h;
     p.counters = c.counters;
+    p.counters_n = (c.flags & ABIN_COUNT_STAGES) ? 3 : 2;
     p.c_out = c.c_out; p.d_out = c.d_out; p.n_out = c.n_out; p.t_out = c.t_out; p.mask_out = c.mask_out;
-    const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * c.n_pages;
     p.stats = stats ? 1 : 0;
     const int w32 = win.w % 32;
-    rc = launch_fast_any(w32, d64, map, p, n_tiles, c.stream);
+    if (use_v4) {
+      // one warp per CTA; a strip = one warp's 32 - KH valid lanes
+      p.n_strips = (int32_t)((c.W + p.Tw - 1) / p.Tw);
+      // strips whose windows stay inside [0, W) (ncol = w) are
+      // [sL, sR); the others take the border variant of the kernel
+      const int64_t Tw = p.Tw;
+      const int64_t sL = std::min<int64_t>(p.n_strips, win.l - 1 > 0 ? (win.l - 1 + Tw - 1) / Tw : 0);
+      const int64_t nfit = (c.W - win.r - Tw) >= 0 ? (c.W - win.r - Tw) / Tw + 1 : 0;
+      p.sL = (int32_t)sL;
+      p.sR = (int32_t)std::max<int64_t>(sL, std::min<int64_t>(nfit, p.n_strips));
+      p.n_pages_v4 = (int32_t)c.n_pages;
+      choose_bands((int64_t)p.n_strips * c.n_pages, c.H_out, win.h, 148 * 16, &p.B, &p.n_bands);
+      const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * c.n_pages;
+      rc = launch_v4_any(w32, d64, map, p, n_tiles, c.stream);
+    } else {
+      const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * c.n_pages;
+      rc = launch_fast_any(w32, d64, map, p, n_tiles, c.stream);
+    }
   } else {
     wide::MomParams p;
     memset(&p, 0, sizeof(p));

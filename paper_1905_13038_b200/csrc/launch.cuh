@@ -8,6 +8,7 @@
 
 #include "moments.cuh"
 #include "moments_wide.cuh"
+#include "moments4.cuh"
 
 namespace abin {
 // warp-strip kernel, w mod 32 = w32 (moments.cuh)
@@ -20,7 +21,9 @@ cudaError_t launch_wide(bool d64, bool stats, int nt, int ph, const CUtensorMap&
 #define ABIN_N_PARTS 8
 #define ABIN_DECL_PART(k)                                                                                 \
   cudaError_t launch_fast_part##k(int w32, bool d64, const CUtensorMap& map, const MomParams& p, int64_t n, \
-                                  cudaStream_t st);
+                                  cudaStream_t st);                                                         \
+  cudaError_t launch_v4_part##k(int w32, bool d64, const CUtensorMap& map, const MomParams& p, int64_t n,   \
+                                cudaStream_t st);
 ABIN_DECL_PART(0) ABIN_DECL_PART(1) ABIN_DECL_PART(2) ABIN_DECL_PART(3)
 ABIN_DECL_PART(4) ABIN_DECL_PART(5) ABIN_DECL_PART(6) ABIN_DECL_PART(7)
 cudaError_t launch_wide_d64(bool d64, bool stats, int nt, int ph, const CUtensorMap& map, const wide::MomParams& p,

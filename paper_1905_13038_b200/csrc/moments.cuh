@@ -62,7 +62,10 @@ struct MomParams {
   float delta1, delta2;      // certified bounds of the two fp32 stages (incl. the fp64 error)
   float inv_h;               // fl(1/h): 1/nrow for interior rows
   int32_t stats;             // statistics mode: every pixel takes the fp64 sequence
-  uint64_t* counters;        // [near_tie, fp64 fallbacks] or null
+  uint64_t* counters;        // [near_tie, fp64 fallbacks(, stage-2 pixels)] or null
+  int32_t counters_n;        // 2, or 3 with ABIN_COUNT_STAGES
+  int32_t sL, sR;            // v4: strips [sL, sR) are interior (no image border inside their windows)
+  int32_t n_pages_v4;        // v4: pages of the launch
   // statistics mode (page 0 only)
   uint64_t* c_out;
   uint64_t* d_out;

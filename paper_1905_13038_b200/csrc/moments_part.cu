@@ -25,7 +25,40 @@ cudaError_t launch_one(const CUtensorMap& map, const MomParams& p, int64_t n_til
   kern<<<(unsigned)n_tiles, kNT, smem, st>>>(map, p);
   return cudaGetLastError();
 }
+template <int W32, bool D64, int METHOD>
+cudaError_t launch_v4_m(const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st) {
+  constexpr size_t smem = v4::smem_bytes();
+  auto kern = v4::k_mom4<W32, D64, METHOD>;
+  static bool attr_set = false;  // benign race: the attribute values are idempotent
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  if (n_tiles > 0) kern<<<(unsigned)n_tiles, 32, smem, st>>>(map, p);
+  return cudaGetLastError();
+}
+
+template <int W32, bool D64>
+cudaError_t launch_v4(const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st) {
+  if (p.method == M_SAUVOLA) return launch_v4_m<W32, D64, M_SAUVOLA>(map, p, n_tiles, st);
+  if (p.method == M_NIBLACK) return launch_v4_m<W32, D64, M_NIBLACK>(map, p, n_tiles, st);
+  return launch_v4_m<W32, D64, M_WOLF>(map, p, n_tiles, st);
+}
 }  // namespace
+
+cudaError_t ABIN_CAT(launch_v4_part, ABIN_PART)(int w32, bool d64, const CUtensorMap& map, const MomParams& p,
+                                                int64_t n, cudaStream_t st) {
+  constexpr int b = 4 * ABIN_PART;
+  switch (w32 - b) {
+    case 0: return d64 ? launch_v4<b + 0, true>(map, p, n, st) : launch_v4<b + 0, false>(map, p, n, st);
+    case 1: return d64 ? launch_v4<b + 1, true>(map, p, n, st) : launch_v4<b + 1, false>(map, p, n, st);
+    case 2: return d64 ? launch_v4<b + 2, true>(map, p, n, st) : launch_v4<b + 2, false>(map, p, n, st);
+    case 3: return d64 ? launch_v4<b + 3, true>(map, p, n, st) : launch_v4<b + 3, false>(map, p, n, st);
+  }
+  return cudaErrorInvalidValue;
+}
 
 cudaError_t ABIN_CAT(launch_fast_part, ABIN_PART)(int w32, bool d64, const CUtensorMap& map, const MomParams& p,
                                                   int64_t n, cudaStream_t st) {
