@@ -81,6 +81,38 @@ constexpr int kZero = kStrip;  // word offset of the zero chunk (columns left of
 #define ABIN_V4_MINB 16  // resident warp-CTAs per SM the register allocation targets
 #endif
 
+// Inclusive warp scan step: v += value of lane - off (if it exists).  The
+// shuffle's predicate output says whether the source lane was in range, so
+// the add is predicated instead of selected.
+__device__ __forceinline__ uint32_t scan_step(uint32_t v, int off) {
+  asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+               "shfl.sync.up.b32 t|p, %0, %1, 0, 0xffffffff;\n\t"
+               "@p add.u32 %0, %0, t;\n\t}"
+               : "+r"(v) : "r"(off));
+  return v;
+}
+__device__ __forceinline__ uint64_t scan_step(uint64_t v, int off) {
+  uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 tl, th;\n\t"
+               "shfl.sync.up.b32 tl|p, %0, %2, 0, 0xffffffff;\n\t"
+               "shfl.sync.up.b32 th, %1, %2, 0, 0xffffffff;\n\t"
+               "@p add.cc.u32 %0, %0, tl;\n\t"
+               "@p addc.u32 %1, %1, th;\n\t}"
+               : "+r"(lo), "+r"(hi) : "r"(off));
+  return ((uint64_t)hi << 32) | lo;
+}
+
+// value of lane `src` (0 if src < 0: columns left of the strip are zero)
+__device__ __forceinline__ uint32_t shfl_idx(uint32_t v, int src) {
+  const uint32_t r = __shfl_sync(0xffffffffu, v, src & 31);
+  return src >= 0 ? r : 0u;
+}
+__device__ __forceinline__ uint64_t shfl_idx(uint64_t v, int src) {
+  const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src & 31);
+  const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src & 31);
+  return src >= 0 ? (((uint64_t)hi << 32) | lo) : 0ull;
+}
+
 template <typename DT>
 __device__ __forceinline__ DT shfl_up(DT v, int off) {
   if constexpr (sizeof(DT) == 8) {
@@ -337,6 +369,7 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
   constexpr int RHO = (kG - W16) % kG;                        // (-w) mod 16
   const int mW = (p.w + RHO) / kG;                            // ceil(w / 16)
   constexpr int method = METHOD;
+  const float delta_amb = slow_all ? __int_as_float(0x7f800000) : p.delta1;  // +inf: every pixel exact
   // rows whose window is clipped by the top / bottom image edge: nrow < h
   const int64_t i_full0 = p.o - 1, i_full1 = p.H_global - 1 - p.u;  // nrow == h for i in [i_full0, i_full1]
 
@@ -354,8 +387,8 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
       const uint4 xo = mask_tail(funnel16<DL>(*reinterpret_cast<const uint4*>(st + kRowsBytes + rr * kSpan),
                                               *reinterpret_cast<const uint4*>(st + kRowsBytes + rr * kSpan + 16)));
       const uint4 xc = xc_next;
-      cptr += p.in_pitch;
-      xc_next = load_centre(cptr, q + 1 < nrows);
+      if (q + 1 < nrows) cptr += p.in_pitch;  // the last row re-reads itself (harmless)
+      xc_next = load_centre(cptr, true);
       // vertical update
 #pragma unroll
       for (int t = 0; t < kG; ++t) {
@@ -388,29 +421,34 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
         td = sd;
 #pragma unroll
         for (int t = RHO; t < kG; ++t) { tc += C[t]; td += (DT)D[t]; }
-        uint32_t ic = tc;
-        DT id = td;
+        if (mW <= 8) {
+          // small windows: sum the m lanes' totals directly -- m + 1 independent
+          // shuffles instead of a dependent 5-level scan
+          uint32_t ac = 0u - shfl_idx(sc, lane - mW);
+          DT ad = (DT)0 - shfl_idx(sd, lane - mW);
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const uint32_t oc = __shfl_up_sync(0xffffffffu, ic, off);
-          const DT od = shfl_up<DT>(id, off);
-          if (lane >= off) { ic += oc; id += od; }
-        }
-        const uint32_t pc = ic - tc;           // P(a_k)
-        const DT pd = id - td;
-        const int src = lane - mW;
-        const uint32_t xc_ = __shfl_sync(0xffffffffu, pc + sc, src & 31);
-        DT xd_;
-        if constexpr (sizeof(DT) == 8) {
-          const uint64_t v = pd + sd;
-          const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src & 31);
-          const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src & 31);
-          xd_ = ((uint64_t)hi << 32) | lo;
+          for (int q = 1; q <= 8; ++q) {
+            if (q > mW) break;
+            ac += shfl_idx(tc, lane - q);
+            ad += shfl_idx(td, lane - q);
+          }
+          Ac = ac;
+          Ad = ad;
         } else {
-          xd_ = __shfl_sync(0xffffffffu, pd + sd, src & 31);
+          uint32_t ic = tc;
+          DT id = td;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            ic = scan_step(ic, off);
+            id = scan_step(id, off);
+          }
+          const uint32_t pc = ic - tc;  // P(a_k)
+          const DT pd = id - td;
+          const uint32_t xc_ = shfl_idx(pc + sc, lane - mW);
+          const DT xd_ = shfl_idx(pd + sd, lane - mW);
+          Ac = pc - xc_;
+          Ad = pd - xd_;
         }
-        Ac = pc - (src >= 0 ? xc_ : 0u);
-        Ad = pd - (src >= 0 ? xd_ : (DT)0);
       }
       // ---- epilogue (Alg. 1 l.118-124, Table 1): row recursion
       // c_t = c_{t-1} + C[a+t] - C[a+t-w] fused with stage 1
@@ -470,7 +508,10 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
             const float2 qn = __fmul2_rn(make_float2(to_f(d0), to_f(dd)), nv);  // -q~
             const float2 vn = __ffma2_rn(mn, mn, qn);                           // -v~
             const float2 sv = make_float2(sqrt_approx(fabsf(vn.x)), sqrt_approx(fabsf(vn.y)));
-            const float2 I = make_float2((float)((wd >> (8 * h2)) & 0xFFu), (float)((wd >> (8 * h2 + 8)) & 0xFFu));
+            // I exactly, off the XU pipe: the byte as the mantissa of 2^23, minus 2^23
+            const float2 I = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(wd, 0x4B000000u, 0x7440u | (uint32_t)h2)),
+                                                    __uint_as_float(__byte_perm(wd, 0x4B000000u, 0x7440u | (uint32_t)(h2 + 1)))),
+                                        make_float2(-8388608.0f, -8388608.0f));
             float2 e;
             if (method == M_SAUVOLA) {
               e = __ffma2_rn(mn, __ffma2_rn(fb2, sv, fa2), I);                                        // I - m g
@@ -491,7 +532,7 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
           wv[g] = ~__byte_perm(lo, hi, 0x7610u) & 0x01010101u;
         }
       }
-      const uint32_t amb = (slow_all || emin < p.delta1) ? vmask : 0u;
+      const uint32_t amb = (emin < delta_amb) ? vmask : 0u;
       if (__any_sync(0xffffffffu, amb != 0u)) {
         uint32_t fix = 0, fixv = 0;
         if (amb)
