@@ -385,7 +385,9 @@ int run_quantile(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int
                  int32_t w, double q, int64_t row0, int64_t H_out, int64_t H_global, int64_t buf_rows,
                  int64_t buf_row0, cudaStream_t st, double* Q_out) {
   const Window win = effective_window(h, w, H_global, W);
-  if (win.w > 8192 || (int64_t)win.h * win.w > 65535) return ABIN_ERANGE;  // u16 bins
+  constexpr int NT_ = 128;
+  if ((int64_t)win.h * win.w > 65535) return ABIN_ERANGE;  // u16 bins
+  if (NT_ + win.w - 1 > 4 * NT_) return ABIN_ERANGE;  // a thread stages at most 4 elements of a row
   constexpr int NT = 128;
   QuantParams p;
   memset(&p, 0, sizeof(p));
