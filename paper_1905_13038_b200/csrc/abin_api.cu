@@ -131,6 +131,7 @@ int launch_wide_any(bool d64, bool stats, int nt, int ph, const CUtensorMap& map
 // double-precision sequence's own error |t_fp64 - t*|.
 struct FilterConsts {
   float fa, fb, delta1, delta2;
+  float rb0, rb1, rdv, rsdv;  // data-dependent stage-1 bound: rb0 + rb1 min(rsdv, rdv / s~)
 };
 
 FilterConsts filter_consts(int method, double k, double R) {
@@ -155,6 +156,16 @@ FilterConsts filter_consts(int method, double k, double R) {
   else { f.fa = (float)k; f.fb = (float)(1.0 / R); }
   f.delta1 = (float)(1.25 * (bound(ds1) + eps64) + 1e-6);
   f.delta2 = (float)(1.25 * (bound(ds2) + eps64) + 1e-6);
+  // The same bound with the data-dependent |s~ - s|: for s0 = sqrt|v~|,
+  // |s0 - s| = |v~ - v| / (s0 + s) <= dv / s0 and s0 >= s~ / (1 + eps_sqrt), so
+  //   |s~ - s| <= min(sqrt dv, dv (1 + eps_sqrt) / s~) + eps_sqrt (128 + sqrt dv).
+  // bound(ds) is affine in ds: bound = b0 + b1 ds.
+  const double b0 = bound(0.0), b1 = bound(1.0) - b0;
+  const double dv = 16.2 * u * qmax;
+  f.rb0 = (float)((1.25 * (b0 + b1 * eps_sqrt * (128.0 + rv) + eps64) + 1e-6) * (1 + 1e-6));
+  f.rb1 = (float)(1.25 * b1 * (1 + 1e-6));
+  f.rdv = (float)(dv * (1 + eps_sqrt) * (1 + 1e-6));
+  f.rsdv = (float)(rv * (1 + 1e-6));
   return f;
 }
 
@@ -315,6 +326,7 @@ int run_moments(const MomCall& c) {
     p.L_page = L8; p.L_fixed = c.L_override;
     const FilterConsts f = filter_consts(c.method, c.k, c.R);
     p.fa = f.fa; p.fb = f.fb; p.delta1 = f.delta1; p.delta2 = f.delta2;
+    p.rb0 = f.rb0; p.rb1 = f.rb1; p.rdv = f.rdv; p.rsdv = f.rsdv;
     p.inv_h = 1.0f / (float)win.h;
     p.counters = c.counters;
     p.counters_n = (c.flags & ABIN_COUNT_STAGES) ? 3 : 2;

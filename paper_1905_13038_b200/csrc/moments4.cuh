@@ -133,13 +133,23 @@ __device__ __forceinline__ float to_f(uint64_t x) {  // x < 2^40 here
 // evaluation in the row loop; both are the same sequence of correctly
 // rounded fp32 operations, so they agree bit for bit).
 __device__ __forceinline__ float stage1_e(int method, float cf, float df, float nu, float I, float fa, float fb,
-                                          float Lf) {
+                                          float Lf, float& sv) {
   const float mn = __fmul_rn(cf, nu);
   const float qn = __fmul_rn(df, nu);
-  const float sv = sqrt_approx(fabsf(__fmaf_rn(mn, mn, qn)));
+  sv = sqrt_approx(fabsf(__fmaf_rn(mn, mn, qn)));
   if (method == M_SAUVOLA) return __fmaf_rn(mn, __fmaf_rn(fb, sv, fa), I);
   if (method == M_NIBLACK) return __fmaf_rn(-fb, sv, __fadd_rn(I, mn));
   return __fmaf_rn(__fmul_rn(-fa, __fadd_rn(mn, Lf)), __fmaf_rn(-fb, sv, 1.0f), __fadd_rn(I, mn));
+}
+
+// The stage-1 bound with the data-dependent |s~ - s| (abin_api.cu
+// filter_consts): rb0 + rb1 min(sqrt dv, dv / s~).  dv / s~ uses the
+// approximate reciprocal (relative error < 2^-22); the 1 + 2^-20 inflation
+// keeps the bound an upper bound.
+__device__ __forceinline__ float refined_bound(const MomParams& p, float s) {
+  float rs;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(s));  // s = 0 -> +inf -> sqrt dv
+  return __fmaf_rn(p.rb1, fminf(p.rsdv, p.rdv * rs), p.rb0) * 1.000001f;
 }
 
 // Rare path (stages 2 and 3) for one lane-row: re-derives c_t, d_t from the
@@ -171,8 +181,12 @@ __device__ __forceinline__ void rare_path(const MomParams& p, const uint32_t* cb
     const uint32_t wd = (t >> 2) == 0 ? xc.x : ((t >> 2) == 1 ? xc.y : ((t >> 2) == 2 ? xc.z : xc.w));
     const uint32_t I = (wd >> (8 * (t & 3))) & 0xFFu;
     if (!slow_all) {
-      const float e = stage1_e(method, to_f(cc), to_f(dd), nu, (float)I, p.fa, p.fb, Lf);
+      float sv;
+      const float e = stage1_e(method, to_f(cc), to_f(dd), nu, (float)I, p.fa, p.fb, Lf, sv);
       if (!(fabsf(e) < p.delta1)) continue;  // stage 1 decided this one
+      // the same bound with the data-dependent |s~ - s|:
+      // the stage-1 sign stands if |e| clears it
+      if (fabsf(e) * 0.999999f >= refined_bound(p, sv)) continue;
     }
     const int64_t j = j0 + t;
     const uint32_t ncol = (uint32_t)max((int64_t)1, min(j + p.r, p.W - 1) - max(j - p.l, (int64_t)-1));
@@ -369,7 +383,6 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
   constexpr int RHO = (kG - W16) % kG;                        // (-w) mod 16
   const int mW = (p.w + RHO) / kG;                            // ceil(w / 16)
   constexpr int method = METHOD;
-  const float delta_amb = slow_all ? __int_as_float(0x7f800000) : p.delta1;  // +inf: every pixel exact
   // rows whose window is clipped by the top / bottom image edge: nrow < h
   const int64_t i_full0 = p.o - 1, i_full1 = p.H_global - 1 - p.u;  // nrow == h for i in [i_full0, i_full1]
 
@@ -461,7 +474,7 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
       }
       const float nu_c = nic_c * inv_nrow;
       uint32_t wv[4];
-      float emin = __int_as_float(0x7f800000);
+      float emin = __int_as_float(0x7f800000), smin = emin;
       {
         uint32_t cc = Ac;
         DT dd = Ad;
@@ -523,6 +536,7 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
               e = __ffma2_rn(ka, b, __fadd2_rn(I, mn));                                              // I - t
             }
             emin = fminf(emin, fminf(fabsf(e.x), fabsf(e.y)));
+            smin = fminf(smin, fminf(sv.x, sv.y));
             e4[h2] = e.x;
             e4[h2 + 1] = e.y;
           }
@@ -532,7 +546,13 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
           wv[g] = ~__byte_perm(lo, hi, 0x7610u) & 0x01010101u;
         }
       }
-      const uint32_t amb = (emin < delta_amb) ? vmask : 0u;
+      // ambiguous lane: some pixel within the certified bound, evaluated with the
+      // lane's smallest s~ (the data-dependent bound decreases in s~)
+      uint32_t amb = slow_all ? vmask : 0u;
+      if (emin < p.delta1) {  // coarse test first (rare for Sauvola)
+        const float dlane = refined_bound(p, smin);
+        if (emin * 0.999999f < dlane) amb = vmask;
+      }
       if (__any_sync(0xffffffffu, amb != 0u)) {
         uint32_t fix = 0, fixv = 0;
         if (amb)
