@@ -14,21 +14,28 @@ __global__ void __launch_bounds__(256) k_global_min(const uint8_t* __restrict__ 
   unsigned int m = 0xFFu;
   const bool vec = ((reinterpret_cast<uintptr_t>(img) | (uintptr_t)pitch | (uintptr_t)W) & 15u) == 0;
   if (vec) {
+    // rows round-robin over the page's blocks, 16-byte chunks across the
+    // threads; four rows in flight per thread (no per-element division)
     const int64_t wq = W >> 4;  // uint4 per row
-    const int64_t nq = H * wq;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nq; e += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t row = e / wq, col = e - row * wq;
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(img + row * pitch) + col);
-      unsigned int x = __vminu4(__vminu4(v.x, v.y), __vminu4(v.z, v.w));
-      x = min(min(x & 0xFFu, (x >> 8) & 0xFFu), min((x >> 16) & 0xFFu, x >> 24));
-      m = min(m, x);
+    for (int64_t row = blockIdx.x; row < H; row += 4 * (int64_t)gridDim.x) {
+      for (int64_t c = threadIdx.x; c < wq; c += blockDim.x) {
+        uint4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t rk = row + (int64_t)k * gridDim.x;
+          v[k] = rk < H ? __ldg(reinterpret_cast<const uint4*>(img + rk * pitch) + c) : make_uint4(~0u, ~0u, ~0u, ~0u);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          unsigned int x = __vminu4(__vminu4(v[k].x, v[k].y), __vminu4(v[k].z, v[k].w));
+          x = min(min(x & 0xFFu, (x >> 8) & 0xFFu), min((x >> 16) & 0xFFu, x >> 24));
+          m = min(m, x);
+        }
+      }
     }
   } else {
-    const int64_t n = H * W;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t row = e / W, col = e - row * W;
-      m = min(m, (unsigned int)img[row * pitch + col]);
-    }
+    for (int64_t row = blockIdx.x; row < H; row += gridDim.x)
+      for (int64_t col = threadIdx.x; col < W; col += blockDim.x) m = min(m, (unsigned int)img[row * pitch + col]);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, off));
