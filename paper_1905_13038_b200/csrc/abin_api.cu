@@ -444,8 +444,9 @@ int run_quantile(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int
 // engines).  The caller's stream waits for all of it.
 struct HostIoStreams {
   int device = -1;
-  cudaStream_t s[3] = {nullptr, nullptr, nullptr};
-  cudaEvent_t done[3] = {nullptr, nullptr, nullptr};
+  static constexpr int kMax = 8;
+  cudaStream_t s[kMax] = {};
+  cudaEvent_t done[kMax] = {};
 };
 
 int get_host_io_streams(HostIoStreams** out) {
@@ -457,7 +458,7 @@ int get_host_io_streams(HostIoStreams** out) {
   std::lock_guard<std::mutex> lock(mu);
   HostIoStreams& h = per_dev[dev];
   if (h.device < 0) {
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < HostIoStreams::kMax; ++i) {
       CK(cudaStreamCreateWithFlags(&h.s[i], cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&h.done[i], cudaEventDisableTiming));
     }
@@ -479,12 +480,17 @@ int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8
   HostIoStreams* hs = nullptr;
   int rc = get_host_io_streams(&hs);
   if (rc) return rc;
-  const int64_t dpitch = (W + 15) / 16 * 16;
+  // device staging keeps the host pitch when it is TMA-friendly, so the copies are linear
+  const int64_t dpitch = (in_pitch % 16 == 0) ? in_pitch : (W + 15) / 16 * 16;
   const int64_t orow = fmt == ABIN_MASK_U8 ? W : (W + 7) / 8;
-  const int64_t dopitch = (orow + 15) / 16 * 16;
+  const int64_t dopitch = (out_pitch % 16 == 0) ? out_pitch : (orow + 15) / 16 * 16;
   const int64_t dpage = dpitch * H, dopage = dopitch * H;
-  int64_t pc = std::max<int64_t>(1, std::min<int64_t>(P, ((int64_t)128 << 20) / std::max<int64_t>(dpage, 1)));
-  const int nstr = (int)std::min<int64_t>(3, (P + pc - 1) / pc);
+  // chunk of pages per stream and the number of streams in flight (tunable
+  // for experiments through ABIN_HOSTIO_CHUNK_MB / ABIN_HOSTIO_STREAMS)
+  static const int64_t chunk_mb = getenv("ABIN_HOSTIO_CHUNK_MB") ? atoll(getenv("ABIN_HOSTIO_CHUNK_MB")) : 64;
+  static const int streams = getenv("ABIN_HOSTIO_STREAMS") ? atoi(getenv("ABIN_HOSTIO_STREAMS")) : 4;
+  int64_t pc = std::max<int64_t>(1, std::min<int64_t>(P, (chunk_mb << 20) / std::max<int64_t>(dpage, 1)));
+  const int nstr = (int)std::min<int64_t>(std::max(1, std::min(streams, (int)HostIoStreams::kMax)), (P + pc - 1) / pc);
   uint8_t* buf = nullptr;
   const size_t per = (size_t)(pc * (dpage + dopage));
   {
@@ -502,7 +508,9 @@ int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8
     cudaStream_t s = hs->s[ci % nstr];
     uint8_t* din = buf + (ci % nstr) * per;
     uint8_t* dout = din + pc * dpage;
-    if (contiguous_in) {
+    if (contiguous_in && in_pitch == dpitch) {  // one linear DMA (2-D copies run at about half the PCIe rate)
+      CK(cudaMemcpyAsync(din, in + c0 * in_page_stride, (size_t)(np * H * dpitch), cudaMemcpyHostToDevice, s));
+    } else if (contiguous_in) {
       CK(cudaMemcpy2DAsync(din, dpitch, in + c0 * in_page_stride, in_pitch, W, np * H, cudaMemcpyHostToDevice, s));
     } else {
       for (int64_t q = 0; q < np; ++q)
@@ -521,7 +529,9 @@ int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8
       rc = run_moments(m);
     }
     if (rc) break;
-    if (contiguous_out) {
+    if (contiguous_out && out_pitch == dopitch) {
+      CK(cudaMemcpyAsync(out + c0 * out_page_stride, dout, (size_t)(np * H * dopitch), cudaMemcpyDeviceToHost, s));
+    } else if (contiguous_out) {
       CK(cudaMemcpy2DAsync(out + c0 * out_page_stride, out_pitch, dout, dopitch, orow, np * H,
                            cudaMemcpyDeviceToHost, s));
     } else {

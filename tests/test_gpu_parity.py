@@ -258,3 +258,29 @@ def test_driver_bands_emulated_on_one_gpu(G, h, w, packed):
     if packed:
         want = oracle.pack_bits(want)
     assert np.array_equal(got, want)
+
+
+# ------------------------------------------------------------ host buffers
+
+@pytest.mark.parametrize("packed,pad", [(False, 0), (True, 0), (False, 5)])
+def test_host_io_batched_equals_device_path(packed, pad):
+    """ABIN_HOST_IO: pinned host pages in, host masks out, streamed through
+    device staging -- identical to the device-resident call (and the oracle)."""
+    P, H, W = 7, 230, 333
+    pages = synth.pages(P, H, W, synth.config_seed(3), stain=True)
+    hbuf = torch.zeros((P, H, W + pad), dtype=torch.uint8).pin_memory()
+    hbuf[:, :, :W] = torch.from_numpy(pages)
+    hin = hbuf[:, :, :W]
+    cols = (W + 7) // 8 if packed else W
+    hout = torch.zeros((P, H, cols + pad), dtype=torch.uint8).pin_memory()
+    fmt = abin.MASK_BITS if packed else abin.MASK_U8
+    rc = abin.raw().abin_binarize_batched(
+        abin.SAUVOLA, abin.ctypes.c_void_p(hin.data_ptr()), hin.stride(0), abin.ctypes.c_void_p(hout.data_ptr()),
+        hout.stride(0), P, H, W, hin.stride(1), hout.stride(1), fmt, 31, 31, 0.5, 128.0, -1, abin.HOST_IO, None,
+        abin.ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    torch.cuda.synchronize()
+    got = hout[:, :, :cols].numpy()
+    for p in range(P):
+        want = oracle.binarize("sauvola", pages[p], 31, 31, 0.5, 128.0)
+        assert np.array_equal(got[p], oracle.pack_bits(want) if packed else want), p
