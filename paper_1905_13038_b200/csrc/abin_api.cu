@@ -225,6 +225,25 @@ void choose_bands(int64_t col_tiles, int64_t H_out, int32_t h, int resident, int
   *n_bands = (int32_t)((H_out + bestB - 1) / bestB);
 }
 
+// v4 (one warp per CTA, tiles of very different cost at the borders): the
+// makespan is about  total work / slots + one tile  (the last wave's tail),
+// with a tile costing its B rows plus h warm-up rows at about half a row each.
+// More, shorter bands shrink the tail; the warm-up rows bound how short.
+void choose_bands_v4(int64_t col_tiles, int64_t H_out, int32_t h, int slots, int32_t* B, int32_t* n_bands) {
+  double best = 1e300;
+  int64_t bestB = H_out;
+  const int64_t nb_max = std::max<int64_t>(1, H_out / 16);
+  for (int64_t nb = 1; nb <= nb_max; ++nb) {
+    const int64_t Bc = (H_out + nb - 1) / nb;
+    const int64_t tiles = col_tiles * ((H_out + Bc - 1) / Bc);
+    const double cost = (double)Bc + 0.5 * h;
+    const double t = (double)tiles * cost / slots + cost;
+    if (t < best * 0.999) { best = t; bestB = Bc; }
+  }
+  *B = (int32_t)bestB;
+  *n_bands = (int32_t)((H_out + bestB - 1) / bestB);
+}
+
 int encode_map(const MomCall& c, int box_rows, bool tma_ok, CUtensorMap* map) {
   memset(map, 0, sizeof(*map));
   if (!tma_ok) return ABIN_OK;
@@ -344,7 +363,12 @@ int run_moments(const MomCall& c) {
       p.sL = (int32_t)sL;
       p.sR = (int32_t)std::max<int64_t>(sL, std::min<int64_t>(nfit, p.n_strips));
       p.n_pages_v4 = (int32_t)c.n_pages;
-      choose_bands((int64_t)p.n_strips * c.n_pages, c.H_out, win.h, 148 * 16, &p.B, &p.n_bands);
+      choose_bands_v4((int64_t)p.n_strips * c.n_pages, c.H_out, win.h, 148 * 16, &p.B, &p.n_bands);
+      if (const char* nb = getenv("ABIN_V4_BANDS")) {  // experiments: force the band count
+        const int64_t want = std::max<int64_t>(1, std::min<int64_t>(atoll(nb), c.H_out));
+        p.B = (int32_t)((c.H_out + want - 1) / want);
+        p.n_bands = (int32_t)((c.H_out + p.B - 1) / p.B);
+      }
       const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * c.n_pages;
       rc = launch_v4_any(w32, d64, map, p, n_tiles, c.stream);
     } else {
