@@ -60,6 +60,8 @@ def _load():
         lib.orc_integral_stats.argtypes = [_P, _I64, _I64, _I64, _I32, _I32, _P, _P]
         lib.orc_quantile.argtypes = [_P, _I64, _I64, _I64, _I32, _I32, _D, _P, _P]
         lib.orc_quantile_points.argtypes = [_P, _I64, _I64, _I64, _I32, _I32, _D, _I64, _P, _P, _P, _P]
+        lib.orc_bernsen.argtypes = [_P, _I64, _I64, _I64, _I32, _I32, _I32, _P, _P, _P]
+        lib.orc_bernsen_points.argtypes = [_P, _I64, _I64, _I64, _I32, _I32, _I32, _I64, _P, _P, _P]
         lib.orc_num_threads.restype = ctypes.c_int
         lib.orc_set_threads.argtypes = [ctypes.c_int]
         _lib = lib
@@ -189,6 +191,31 @@ def quantile_points(I, h: int, w: int, q: float, rows, cols):
                                    cols.ctypes.data, mask.ctypes.data, Q.ctypes.data) != 0:
         raise MemoryError
     return mask, Q
+
+
+def bernsen(I, h: int, w: int, contrast: int = -1):
+    """Bernsen midrange rule: mask 0 iff 2 I <= min + max of the
+    in-bounds window; contrast >= 0: background where max - min < contrast.
+    Returns (mask, min, max)."""
+    I = _img(I)
+    H, W = I.shape
+    mask = np.empty((H, W), np.uint8)
+    lo = np.empty((H, W), np.uint8)
+    hi = np.empty((H, W), np.uint8)
+    _load().orc_bernsen(I.ctypes.data, H, W, I.strides[0], h, w, contrast, mask.ctypes.data, lo.ctypes.data,
+                        hi.ctypes.data)
+    return mask, lo, hi
+
+
+def bernsen_points(I, h: int, w: int, contrast: int, rows, cols):
+    I = _img(I)
+    H, W = I.shape
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    cols = np.ascontiguousarray(cols, dtype=np.int64)
+    mask = np.empty(rows.size, np.uint8)
+    _load().orc_bernsen_points(I.ctypes.data, H, W, I.strides[0], h, w, contrast, rows.size, rows.ctypes.data,
+                               cols.ctypes.data, mask.ctypes.data)
+    return mask
 
 
 def pack_bits(mask: np.ndarray) -> np.ndarray:

@@ -337,3 +337,60 @@ int orc_quantile_points(const uint8_t *I, int64_t H, int64_t W, int64_t pitch, i
   }
   return rc;
 }
+
+/* ---- Bernsen: local midrange (Sec. 3.4 "Generalization") ----
+ * min and max of the in-bounds gray levels of the window (rows (i-o, i+u],
+ * cols (j-l, j+r], out-of-bounds pixels excluded -- the extrema of the
+ * pixels that exist), threshold t = (min + max) / 2 ("used midrange as
+ * threshold value"), foreground iff I <= t.  With integer gray levels,
+ * I <= (min + max)/2  <=>  2 I <= min + max, evaluated exactly.
+ * contrast >= 0 selects the local-contrast variant the same paragraph
+ * mentions ("estimate local contrast by range of gray levels"): a pixel whose
+ * window range max - min is below `contrast` is background (1); otherwise the
+ * midrange rule (SPEC threshold-rules, rule bernsen-contrast).  The direct
+ * definition: Theta(h w) per pixel. */
+static void direct_extrema(const uint8_t *I, int64_t H, int64_t W, int64_t pitch, int32_t h, int32_t w, int64_t i,
+                           int64_t j, int32_t *mn_out, int32_t *mx_out) {
+  int64_t l, r, o, u;
+  offsets(h, w, &l, &r, &o, &u);
+  int32_t lo = 255, hi = 0;
+  for (int64_t a = mx(i - o + 1, 0); a <= mn(i + u, H - 1); ++a)
+    for (int64_t b = mx(j - l + 1, 0); b <= mn(j + r, W - 1); ++b) {
+      const int32_t x = I[a * pitch + b];
+      if (x < lo) lo = x;
+      if (x > hi) hi = x;
+    }
+  *mn_out = lo;
+  *mx_out = hi;
+}
+
+static uint8_t bernsen_decide(int32_t x, int32_t lo, int32_t hi, int32_t contrast) {
+  if (contrast >= 0 && hi - lo < contrast) return 1; /* low contrast: background */
+  return (2 * x <= lo + hi) ? 0 : 1;
+}
+
+int orc_bernsen(const uint8_t *I, int64_t H, int64_t W, int64_t pitch, int32_t h, int32_t w, int32_t contrast,
+                uint8_t *mask, uint8_t *min_out, uint8_t *max_out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < H; ++i)
+    for (int64_t j = 0; j < W; ++j) {
+      int32_t lo, hi;
+      direct_extrema(I, H, W, pitch, h, w, i, j, &lo, &hi);
+      if (mask) mask[i * W + j] = bernsen_decide(I[i * pitch + j], lo, hi, contrast);
+      if (min_out) min_out[i * W + j] = (uint8_t)lo;
+      if (max_out) max_out[i * W + j] = (uint8_t)hi;
+    }
+  return 0;
+}
+
+int orc_bernsen_points(const uint8_t *I, int64_t H, int64_t W, int64_t pitch, int32_t h, int32_t w,
+                       int32_t contrast, int64_t m, const int64_t *rows, const int64_t *cols, uint8_t *mask) {
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t q = 0; q < m; ++q) {
+    int32_t lo, hi;
+    direct_extrema(I, H, W, pitch, h, w, rows[q], cols[q], &lo, &hi);
+    mask[q] = bernsen_decide(I[rows[q] * pitch + cols[q]], lo, hi, contrast);
+  }
+  return 0;
+}
+

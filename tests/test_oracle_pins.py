@@ -337,3 +337,57 @@ def test_oracle_compiled_without_fma_contraction():
     # The canonical double sequence must not be contracted into FMAs.
     out = subprocess.run(["objdump", "-d", oracle.build()], capture_output=True, text=True).stdout
     assert "vfmadd" not in out and "vfmsub" not in out and "vfnmadd" not in out
+
+
+# ---------------------------------------------------------------- Bernsen
+
+def _brute_extrema(I, h, w, i, j):
+    """Enumerate the real-valued window of PAPER.md:27 directly (independent
+    of the oracle's offsets) and take min / max of the in-bounds pixels."""
+    H, W = I.shape
+    vals = [int(I[a, b]) for a in range(H) for b in range(W)
+            if i - h / 2 < a <= i + h / 2 and j - w / 2 < b <= j + w / 2]
+    return min(vals), max(vals)
+
+
+def test_bernsen_extrema_brute_force():
+    rng = np.random.default_rng(11)
+    for (H, W), (h, w) in [((7, 9), (3, 3)), ((8, 5), (4, 2)), ((6, 11), (5, 6)), ((5, 5), (9, 9)), ((9, 4), (1, 7))]:
+        I = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+        mask, lo, hi = oracle.bernsen(I, h, w)
+        for i in range(H):
+            for j in range(W):
+                a, b = _brute_extrema(I, h, w, i, j)
+                assert (lo[i, j], hi[i, j]) == (a, b)
+                # midrange decision as a rational comparison: I <= (min+max)/2
+                assert mask[i, j] == (0 if Fraction(int(I[i, j])) <= Fraction(a + b, 2) else 1)
+
+
+def test_bernsen_matches_quantile_extremes():
+    # min = rho-th smallest with rho = 1 (q -> 0), max = q = 1 (SPEC quantile
+    # convention) -- the sort-based quantile oracle is an independent path
+    I = synth.page(40, 57, synth.config_seed(5, 3))
+    _, lo, hi = oracle.bernsen(I, 9, 7)
+    _, qmin = oracle.quantile(I, 9, 7, 1e-9)
+    _, qmax = oracle.quantile(I, 9, 7, 1.0)
+    assert np.array_equal(lo, qmin) and np.array_equal(hi, qmax)
+
+
+def test_bernsen_closed_forms():
+    # constant image: min = max = g = I, I <= g -> all foreground; with any
+    # positive contrast threshold the range 0 is "low contrast" -> background
+    I = synth.constant(13, 17, 77)
+    assert (oracle.bernsen(I, 5, 5)[0] == 0).all()
+    assert (oracle.bernsen(I, 5, 5, contrast=1)[0] == 1).all()
+    # 1x1 window: min = max = I -> foreground everywhere
+    J = synth.uniform_random(10, 12, 4)
+    assert (oracle.bernsen(J, 1, 1)[0] == 0).all()
+    # threshold within [min, max] (SPEC threshold-rules): min <= I always, so
+    # the window minimum itself is always foreground
+    m, lo, hi = oracle.bernsen(J, 3, 3)
+    assert (lo <= hi).all()
+    assert ((J == lo) <= (m == 0)).all()
+    # whole-image window: global midrange
+    m, lo, hi = oracle.bernsen(J, 2 * 10 + 1, 2 * 12 + 1)
+    assert (lo == J.min()).all() and (hi == J.max()).all()
+    assert np.array_equal(m, (2 * J.astype(int) > int(J.min()) + int(J.max())).astype(np.uint8))
