@@ -121,13 +121,23 @@ int abin_wolf(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t
 int abin_quantile(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out, int64_t out_pitch,
                   int32_t mask_format, int32_t h, int32_t w, double q, uint32_t flags, void* stream);
 
+/* ---- Bernsen's midrange rule ----------------------------------
+ * min, max = extrema of the in-bounds gray levels of the window; I' = 0 iff
+ * I <= (min + max) / 2 (exact integer test 2 I <= min + max).  contrast >= 0
+ * selects the local-contrast variant (same paragraph: "estimate local contrast
+ * by range of gray levels"): I' = 1 where max - min < contrast.  Computed from
+ * the sliding-histogram kernel of abin_quantile. */
+int abin_bernsen(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out, int64_t out_pitch,
+                 int32_t mask_format, int32_t h, int32_t w, int32_t contrast, uint32_t flags, void* stream);
+
 /* ---- Page batches ------------------------------------------------------------
  * n_pages pages of identical H x W geometry; page p is read at
  * in + p * in_page_stride and written at out + p * out_page_stride (bytes).
  * method: 0 Sauvola, 1 Niblack, 2 Wolf (per-page L unless L_override >= 0),
- * 3 quantile (param0 = q).  param0 = k (or q), param1 = R.
+ * 3 quantile (param0 = q), 4 Bernsen (param0 = contrast, < 0: plain midrange).
+ * param0 = k (or q, contrast), param1 = R.
  * With ABIN_HOST_IO, in/out are host pointers. */
-enum { ABIN_SAUVOLA = 0, ABIN_NIBLACK = 1, ABIN_WOLF = 2, ABIN_QUANTILE = 3 };
+enum { ABIN_SAUVOLA = 0, ABIN_NIBLACK = 1, ABIN_WOLF = 2, ABIN_QUANTILE = 3, ABIN_BERNSEN = 4 };
 int abin_binarize_batched(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8_t* out,
                           int64_t out_page_stride, int64_t n_pages, int64_t H, int64_t W, int64_t in_pitch,
                           int64_t out_pitch, int32_t mask_format, int32_t h, int32_t w, double param0,
@@ -159,7 +169,8 @@ int abin_global_min(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, 
  *   t_out         double threshold (the exact fp64 sequence, every pixel);
  *   mask_out      uint8 mask (ABIN_MASK_U8 layout, pitch W).
  * method 0..2 as above (L_override as for Wolf).  For method 3 (quantile)
- * t_out receives Q as a double and c_out/d_out are not written. */
+ * t_out receives Q as a double, for method 4 (Bernsen) the midrange
+ * (min + max) / 2; c_out/d_out/n_out are not written for methods 3, 4. */
 int abin_stats(int32_t method, const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, int32_t h, int32_t w,
                double param0, double param1, int32_t L_override, uint64_t* c_out, uint64_t* d_out,
                uint32_t* n_out, double* t_out, uint8_t* mask_out, void* stream);

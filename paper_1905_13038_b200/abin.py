@@ -25,8 +25,8 @@ _I32 = ctypes.c_int32
 _U32 = ctypes.c_uint32
 _D = ctypes.c_double
 
-SAUVOLA, NIBLACK, WOLF, QUANTILE = 0, 1, 2, 3
-METHODS = {"sauvola": SAUVOLA, "niblack": NIBLACK, "wolf": WOLF, "quantile": QUANTILE}
+SAUVOLA, NIBLACK, WOLF, QUANTILE, BERNSEN = 0, 1, 2, 3, 4
+METHODS = {"sauvola": SAUVOLA, "niblack": NIBLACK, "wolf": WOLF, "quantile": QUANTILE, "bernsen": BERNSEN}
 MASK_U8, MASK_BITS = 0, 1
 FORCE_U64_SQ, FORCE_FP64, HOST_IO, COUNT_STAGES = 1, 2, 4, 8
 V3_INTERNAL = 1 << 29  # internal test hook: the 4-warp-CTA kernel instead of the warp-CTA kernel
@@ -36,6 +36,7 @@ _lib.abin_sauvola.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, 
 _lib.abin_niblack.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _D, _U32, _P, _P]
 _lib.abin_wolf.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _D, _D, _I32, _U32, _P, _P]
 _lib.abin_quantile.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _D, _U32, _P]
+_lib.abin_bernsen.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _I32, _U32, _P]
 _lib.abin_binarize_batched.argtypes = [_I32, _P, _I64, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _D,
                                        _D, _I32, _U32, _P, _P]
 _lib.abin_binarize_band.argtypes = [_I32, _P, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _P, _I64, _I32, _I32, _I32,
@@ -54,7 +55,7 @@ class AbinLimits(ctypes.Structure):
 
 _lib.abin_limits.argtypes = [ctypes.POINTER(AbinLimits)]
 
-EXPORTED = ["abin_sauvola", "abin_niblack", "abin_wolf", "abin_quantile", "abin_binarize_batched",
+EXPORTED = ["abin_sauvola", "abin_niblack", "abin_wolf", "abin_quantile", "abin_bernsen", "abin_binarize_batched",
             "abin_binarize_band", "abin_global_min", "abin_stats", "abin_limits", "abin_strerror", "abin_version",
             "abin_last_cuda_error"]
 
@@ -147,6 +148,17 @@ def quantile(img: torch.Tensor, h: int, w: int, q: float = 0.5, packed: bool = F
     return out
 
 
+def bernsen(img: torch.Tensor, h: int, w: int, contrast: int = -1, packed: bool = False, out=None, flags: int = 0,
+            stream=None) -> torch.Tensor:
+    """Bernsen midrange rule: mask 0 iff 2 I <= min + max of
+    the window; contrast >= 0: 1 where max - min < contrast."""
+    H, W, pitch = _img2d(img)
+    out = _alloc_mask(H, W, packed, img.device) if out is None else out
+    _check(_lib.abin_bernsen(_ptr(img), H, W, pitch, _ptr(out), out.stride(0), MASK_BITS if packed else MASK_U8, h,
+                             w, contrast, flags, _stream(stream)))
+    return out
+
+
 def binarize_batched(method: str, pages: torch.Tensor, h: int, w: int, param0: float, param1: float = 128.0,
                      L: int = -1, packed: bool = False, out=None, flags: int = 0, counters: torch.Tensor = None,
                      stream=None) -> torch.Tensor:
@@ -196,7 +208,7 @@ def stats(method: str, img: torch.Tensor, h: int, w: int, param0: float, param1:
     n = torch.empty((H, W), dtype=torch.int32, device=dev)
     t = torch.empty((H, W), dtype=torch.float64, device=dev)
     m = torch.empty((H, W), dtype=torch.uint8, device=dev)
-    quant = method == "quantile"
+    quant = method in ("quantile", "bernsen")
     _check(_lib.abin_stats(METHODS[method], _ptr(img), H, W, pitch, h, w, param0, param1, L, None if quant else _ptr(c),
                            None if quant else _ptr(d), None if quant else _ptr(n), _ptr(t), _ptr(m), _stream(stream)))
     out = {"t": t, "mask": m}

@@ -408,15 +408,16 @@ int run_moments(const MomCall& c) {
 
 int check_params(int32_t method, double p0, double p1) {
   if (method == ABIN_QUANTILE) return (std::isfinite(p0) && p0 > 0.0 && p0 <= 1.0) ? ABIN_OK : ABIN_EINVAL;
+  if (method == ABIN_BERNSEN) return std::isfinite(p0) ? ABIN_OK : ABIN_EINVAL;  // contrast (< 0: plain midrange)
   if (!std::isfinite(p0)) return ABIN_EINVAL;
   if (method == ABIN_SAUVOLA || method == ABIN_WOLF)
     if (!std::isfinite(p1) || !(p1 > 0.0)) return ABIN_EINVAL;
-  if (method < 0 || method > 3) return ABIN_EINVAL;
+  if (method < 0 || method > 4) return ABIN_EINVAL;
   return ABIN_OK;
 }
 
 
-int run_quantile(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64_t /*H_held*/, int64_t W,
+int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64_t /*H_held*/, int64_t W,
                  int64_t in_pitch, uint8_t* out, int64_t out_pitch, int64_t out_page_stride, int32_t fmt, int32_t h,
                  int32_t w, double q, int64_t row0, int64_t H_out, int64_t H_global, int64_t buf_rows,
                  int64_t buf_row0, cudaStream_t st, double* Q_out) {
@@ -450,13 +451,16 @@ int run_quantile(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int
   p.n_bands = (int32_t)((H_out + B - 1) / B);
   p.Q_out = Q_out;
   const size_t smem = quantile_smem_bytes(NT, win.w);
+  p.contrast = method == ABIN_BERNSEN ? (int32_t)std::max(-1.0, std::min(256.0, std::floor(q))) : -1;
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(k_quantile<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    CK(cudaFuncSetAttribute(k_quantile<NT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    CK(cudaFuncSetAttribute(k_quantile<NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
   const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * n_pages;
-  k_quantile<NT><<<(unsigned)n_tiles, NT, smem, st>>>(p);
+  if (method == ABIN_BERNSEN) k_quantile<NT, 1><<<(unsigned)n_tiles, NT, smem, st>>>(p);
+  else k_quantile<NT, 0><<<(unsigned)n_tiles, NT, smem, st>>>(p);
   CK(cudaGetLastError());
   return ABIN_OK;
 }
@@ -493,7 +497,7 @@ int get_host_io_streams(HostIoStreams** out) {
 }
 
 int run_moments(const MomCall& c);
-int run_quantile(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64_t H_held, int64_t W,
+int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64_t H_held, int64_t W,
                  int64_t in_pitch, uint8_t* out, int64_t out_pitch, int64_t out_page_stride, int32_t fmt, int32_t h,
                  int32_t w, double q, int64_t row0, int64_t H_out, int64_t H_global, int64_t buf_rows,
                  int64_t buf_row0, cudaStream_t st, double* Q_out);
@@ -541,8 +545,8 @@ int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8
         CK(cudaMemcpy2DAsync(din + q * dpage, dpitch, in + (c0 + q) * in_page_stride, in_pitch, W, H,
                              cudaMemcpyHostToDevice, s));
     }
-    if (method == ABIN_QUANTILE) {
-      rc = run_quantile(din, dpage, np, H, W, dpitch, dout, dopitch, dopage, fmt, h, w, p0, 0, H, H, H, 0, s, nullptr);
+    if (method == ABIN_QUANTILE || method == ABIN_BERNSEN) {
+      rc = run_quantile(method, din, dpage, np, H, W, dpitch, dout, dopitch, dopage, fmt, h, w, p0, 0, H, H, H, 0, s, nullptr);
     } else {
       MomCall m;
       memset(&m, 0, sizeof(m));
@@ -598,8 +602,8 @@ int abin_binarize_batched(int32_t method, const uint8_t* in, int64_t in_page_str
   if (flags & ABIN_HOST_IO)
     return run_host_io(method, in, in_page_stride, out, out_page_stride, n_pages, H, W, in_pitch, out_pitch,
                        mask_format, h, w, param0, param1, L_override, flags, counters, st);
-  if (method == ABIN_QUANTILE)
-    return run_quantile(in, in_page_stride, n_pages, H, W, in_pitch, out, out_pitch, out_page_stride, mask_format, h,
+  if (method == ABIN_QUANTILE || method == ABIN_BERNSEN)
+    return run_quantile(method, in, in_page_stride, n_pages, H, W, in_pitch, out, out_pitch, out_page_stride, mask_format, h,
                         w, param0, 0, H, H, H, 0, st, nullptr);
   MomCall c;
   memset(&c, 0, sizeof(c));
@@ -656,6 +660,12 @@ int abin_quantile(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uin
                                0.0, -1, flags, nullptr, stream);
 }
 
+int abin_bernsen(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out, int64_t out_pitch,
+                 int32_t mask_format, int32_t h, int32_t w, int32_t contrast, uint32_t flags, void* stream) {
+  return abin_binarize_batched(ABIN_BERNSEN, in, 0, out, 0, 1, H, W, in_pitch, out_pitch, mask_format, h, w,
+                               (double)contrast, 0.0, -1, flags, nullptr, stream);
+}
+
 int abin_binarize_band(int32_t method, const uint8_t* in, int64_t H_band, int64_t W, int64_t in_pitch, int64_t row0,
                        int64_t H_global, int32_t halo_top, int32_t halo_bot, uint8_t* out, int64_t out_pitch,
                        int32_t mask_format, int32_t h, int32_t w, double param0, double param1, int32_t L_override,
@@ -674,8 +684,8 @@ int abin_binarize_band(int32_t method, const uint8_t* in, int64_t H_band, int64_
   const int64_t out_row = mask_format == ABIN_MASK_U8 ? W : (W + 7) / 8;
   if (overlaps(in, (size_t)in_bytes, out, (size_t)((H_band - 1) * out_pitch + out_row))) return ABIN_EALIAS;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (method == ABIN_QUANTILE)
-    return run_quantile(in, 0, 1, held, W, in_pitch, out, out_pitch, 0, mask_format, h, w, param0, row0, H_band,
+  if (method == ABIN_QUANTILE || method == ABIN_BERNSEN)
+    return run_quantile(method, in, 0, 1, held, W, in_pitch, out, out_pitch, 0, mask_format, h, w, param0, row0, H_band,
                         H_global, held, row0 - halo_top, st, nullptr);
   MomCall c;
   memset(&c, 0, sizeof(c));
@@ -729,8 +739,8 @@ int abin_stats(int32_t method, const uint8_t* in, int64_t H, int64_t W, int64_t 
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* scratch = nullptr;  // the mask also goes to a throwaway U8 buffer
   CK(cudaMallocAsync(&scratch, (size_t)(H * W), st));
-  if (method == ABIN_QUANTILE) {
-    rc = run_quantile(in, 0, 1, H, W, in_pitch, scratch, W, 0, ABIN_MASK_U8, h, w, param0, 0, H, H, H, 0, st, t_out);
+  if (method == ABIN_QUANTILE || method == ABIN_BERNSEN) {
+    rc = run_quantile(method, in, 0, 1, H, W, in_pitch, scratch, W, 0, ABIN_MASK_U8, h, w, param0, 0, H, H, H, 0, st, t_out);
   } else {
     MomCall c;
     memset(&c, 0, sizeof(c));
@@ -759,7 +769,7 @@ int abin_stats(int32_t method, const uint8_t* in, int64_t H, int64_t W, int64_t 
     c.mask_out = mask_out;
     rc = run_moments(c);
   }
-  if (mask_out && method == ABIN_QUANTILE && rc == ABIN_OK) {
+  if (mask_out && (method == ABIN_QUANTILE || method == ABIN_BERNSEN) && rc == ABIN_OK) {
     cudaError_t e = cudaMemcpyAsync(mask_out, scratch, (size_t)(H * W), cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) rc = cuda_fail(e);
   }

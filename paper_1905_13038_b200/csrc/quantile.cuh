@@ -19,6 +19,12 @@
 // The quantile itself is tracked incrementally: below = #(x < Q) follows every
 // update, and Q moves by the few bins the row changed.  Out-of-bounds pixels
 // are excluded (not zero-padded).
+//
+// MODE 1 is Bernsen's midrange rule: the same histograms give
+// the window extrema -- the minimum / maximum are tracked from the added
+// values and walked inward past emptied bins -- and the decision
+// I <= (min + max) / 2 is the exact integer test 2 I <= min + max (with the
+// local-contrast variant: background where max - min < contrast).
 #pragma once
 #include <cstdint>
 #include <cmath>
@@ -37,7 +43,8 @@ struct QuantParams {
   int32_t h, w, l, r, o, u;
   double q;
   int32_t B, n_bands, n_strips;
-  double* Q_out;  // optional (page 0): Q per pixel as double
+  double* Q_out;  // optional (page 0): Q (Bernsen: the midrange) per pixel as double
+  int32_t contrast;  // Bernsen: < 0 plain midrange, else background where max - min < contrast
 };
 
 // A staged pixel's bin code (uint2): x = byte offset of its bin's word in the
@@ -53,7 +60,7 @@ __device__ __forceinline__ uint2 skip_code() {
   return make_uint2(128u * (uint32_t)(NT * 4), 255u << 24);
 }
 
-template <int NT>
+template <int NT, int MODE>
 __global__ void __launch_bounds__(NT) k_quantile(const QuantParams p) {
   extern __shared__ __align__(16) uint8_t qsm[];
   uint32_t* hist = reinterpret_cast<uint32_t*>(qsm);                        // [129][NT] packed u16 bins (+trash)
@@ -108,6 +115,7 @@ __global__ void __launch_bounds__(NT) k_quantile(const QuantParams p) {
   };
 
   int Q = 0, below = 0;  // below = #(x < Q) over the window
+  int lo = 255, hi = 0;  // MODE 1: bounds on the window extrema (lo <= min, hi >= max)
   // warm-up: rows y0-o .. y0+u-1 (the first main step adds y0+u, removes y0-o)
   {
     int raw[KS];
@@ -122,6 +130,7 @@ __global__ void __launch_bounds__(NT) k_quantile(const QuantParams p) {
         for (int e = s0; e <= s1; ++e) {
           const uint2 c = codes[e];
           atom_add(hb + c.x, c.y & 0xFFFFFFu);
+          if (MODE == 1 && (c.y & 0xFFFFFFu)) { lo = min(lo, (int)(c.y >> 24)); hi = max(hi, (int)(c.y >> 24)); }
         }
       }
     }
@@ -151,6 +160,8 @@ __global__ void __launch_bounds__(NT) k_quantile(const QuantParams p) {
     uint8_t mk = 0;
     int Qv = 0;
     if (active) {
+      auto cnt = [&](int g) { return (int)((hist[(g >> 1) * NT + t] >> ((g & 1) << 4)) & 0xFFFFu); };
+      if (MODE == 0) {
       const uint32_t qk = (uint32_t)Q << 24;  // y < qk  <=>  v < Q
       int dbelow = 0;
 #pragma unroll 4
@@ -161,12 +172,28 @@ __global__ void __launch_bounds__(NT) k_quantile(const QuantParams p) {
         dbelow += (int)(a.y < qk) - (int)(b.y < qk);
       }
       below += dbelow;
+      } else {
+#pragma unroll 4
+        for (int e = s0; e <= s1; ++e) {
+          const uint2 a = c_in[e], b = c_out[e];
+          atom_add(hb + a.x, a.y & 0xFFFFFFu);
+          atom_add(hb + b.x, 0u - (b.y & 0xFFFFFFu));
+          const int va = (int)(a.y >> 24);
+          if (a.y & 0xFFFFFFu) { lo = min(lo, va); hi = max(hi, va); }
+        }
+        // removals may have emptied the extreme bins: walk inward (n >= 1)
+        while (cnt(lo) == 0) ++lo;
+        while (cnt(hi) == 0) --hi;
+        if (p.contrast >= 0 && hi - lo < p.contrast) mk = 1;  // low local contrast: background
+        else mk = (2 * I <= lo + hi) ? 0 : 1;
+        if (p.Q_out && page == 0) p.Q_out[(i - p.row0) * p.W + j] = 0.5 * (double)(lo + hi);
+      }
+      if (MODE == 0) {
       const int nrow = (int)(min(i + p.u, p.H_global - 1) - max(i - p.o, (int64_t)-1));
       const int n = ncol * nrow;
       int rho = (int)ceil(__dmul_rn(p.q, (double)n));
       if (rho < 1) rho = 1;
       // rank tracking: restore below < rho <= below + count(Q)
-      auto cnt = [&](int g) { return (int)((hist[(g >> 1) * NT + t] >> ((g & 1) << 4)) & 0xFFFFu); };
       while (below >= rho) {
         --Q;
         below -= cnt(Q);
@@ -177,6 +204,7 @@ __global__ void __launch_bounds__(NT) k_quantile(const QuantParams p) {
       }
       mk = (I <= Q) ? 0 : 1;
       Qv = Q;
+      }
     }
     if (p.fmt == 0) {
       if (active) orow[j] = mk;
@@ -190,7 +218,7 @@ __global__ void __launch_bounds__(NT) k_quantile(const QuantParams p) {
         orow[j >> 3] = (uint8_t)byte;
       }
     }
-    if (p.Q_out && page == 0 && active) p.Q_out[(i - p.row0) * p.W + j] = (double)Qv;
+    if (MODE == 0 && p.Q_out && page == 0 && active) p.Q_out[(i - p.row0) * p.W + j] = (double)Qv;
   }
 }
 

@@ -144,3 +144,16 @@ def test_config5_quantile_sampled(q):
         rows, cols = sample_points(H, W, 30_000, seed=int(q * 10) + p, seam=128)
         mref, _ = oracle.quantile_points(host[p], 51, 51, q, rows, cols)
         assert np.array_equal(m[p][rows, cols], mref), (q, p)
+
+
+def test_bernsen_fullsize_sampled():
+    """Bernsen (NEXT #1) on a config-5-sized page (4096 x 4096, 51 x 51) and a
+    16-page batch, sampled pixels vs the direct extrema oracle."""
+    H = W = 4096
+    host, x = device_pages(16, H, W, 5, True)
+    for contrast in (-1, 20):
+        m = ab.binarize_batched("bernsen", x, 51, 51, float(contrast)).cpu().numpy()
+        for p in (0, 15):
+            rows, cols = sample_points(H, W, 30_000, seed=p + contrast, seam=128)
+            ref = oracle.bernsen_points(host[p], 51, 51, contrast, rows, cols)
+            assert np.array_equal(m[p][rows, cols], ref), (contrast, p)

@@ -284,3 +284,47 @@ def test_host_io_batched_equals_device_path(packed, pad):
     for p in range(P):
         want = oracle.binarize("sauvola", pages[p], 31, 31, 0.5, 128.0)
         assert np.array_equal(got[p], oracle.pack_bits(want) if packed else want), p
+
+
+# ------------------------------------------------------------ Bernsen (NEXT #1)
+
+@pytest.mark.parametrize("contrast", [-1, 15])
+def test_bernsen_small(contrast):
+    """Bernsen midrange on the histogram kernel vs the direct
+    extrema oracle: random and document images, odd/even windows, windows
+    larger than the image, byte and bit masks, tight and padded pitches."""
+    rng = np.random.default_rng(contrast + 2)
+    cases = [((33, 41), (5, 5)), ((64, 200), (51, 51)), ((7, 300), (4, 9)), ((100, 3), (3, 100)),
+             ((130, 257), (16, 31))]
+    for (H, W), (h, w) in cases:
+        for I in (rng.integers(0, 256, size=(H, W), dtype=np.uint8),
+                  synth.page(H, W, synth.config_seed(6, H), stain=True)):
+            ref, lo, hi = oracle.bernsen(I, h, w, contrast)
+            for pitch in (None, W):
+                x = to_dev(I, pitch)
+                assert np.array_equal(ab.bernsen(x, h, w, contrast).cpu().numpy(), ref)
+                assert np.array_equal(ab.bernsen(x, h, w, contrast, packed=True).cpu().numpy(), oracle.pack_bits(ref))
+            s = ab.stats("bernsen", to_dev(I), h, w, float(contrast))
+            assert np.array_equal(s["t"].cpu().numpy(), 0.5 * (lo.astype(np.float64) + hi))
+            assert np.array_equal(s["mask"].cpu().numpy(), ref)
+
+
+def test_bernsen_constant_and_bands():
+    I = synth.constant(50, 70, 91)
+    assert (ab.bernsen(to_dev(I), 9, 9).cpu().numpy() == 0).all()
+    assert (ab.bernsen(to_dev(I), 9, 9, contrast=1).cpu().numpy() == 1).all()
+    J = synth.page(600, 400, synth.config_seed(6, 1))
+    whole, _, _ = oracle.bernsen(J, 21, 21, 20)
+    for G in (2, 5):
+        bounds = np.linspace(0, 600, G + 1).astype(int)
+        parts = []
+        for g in range(G):
+            r0, r1 = bounds[g], bounds[g + 1]
+            top, bot = min(10, r0), min(10, 600 - r1)
+            held = to_dev(np.ascontiguousarray(J[r0 - top:r1 + bot]))
+            parts.append(ab.binarize_band("bernsen", held, r0, 600, top, bot, 21, 21, 20.0).cpu().numpy())
+        assert np.array_equal(np.concatenate(parts), whole)
+    P = synth.pages(3, 90, 130, synth.config_seed(6, 2))
+    mb = ab.binarize_batched("bernsen", torch.from_numpy(P).to(DEV), 15, 15, -1.0).cpu().numpy()
+    for p in range(3):
+        assert np.array_equal(mb[p], oracle.bernsen(P[p], 15, 15)[0])
