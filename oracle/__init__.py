@@ -62,6 +62,11 @@ def _load():
         lib.orc_quantile_points.argtypes = [_P, _I64, _I64, _I64, _I32, _I32, _D, _I64, _P, _P, _P, _P]
         lib.orc_bernsen.argtypes = [_P, _I64, _I64, _I64, _I32, _I32, _I32, _P, _P, _P]
         lib.orc_bernsen_points.argtypes = [_P, _I64, _I64, _I64, _I32, _I32, _I32, _I64, _P, _P, _P]
+        lib.orc_threshold_rule.argtypes = [_I32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _P, _D, _D, _D,
+                                           _D]
+        lib.orc_threshold_rule.restype = _D
+        lib.orc_global_mean_std.argtypes = [_P, _I64, _I64, _I64, _P, _P]
+        lib.orc_binarize_rule.argtypes = [_I32, _P, _I64, _I64, _I64, _I32, _I32, _P, _I64, _P, _P, _P, _P]
         lib.orc_num_threads.restype = ctypes.c_int
         lib.orc_set_threads.argtypes = [ctypes.c_int]
         _lib = lib
@@ -216,6 +221,43 @@ def bernsen_points(I, h: int, w: int, contrast: int, rows, cols):
     _load().orc_bernsen_points(I.ctypes.data, H, W, I.strides[0], h, w, contrast, rows.size, rows.ctypes.data,
                                cols.ctypes.data, mask.ctypes.data)
     return mask
+
+
+RULES = {"feng": 5, "rais": 6, "khurshid": 7, "phansalkar": 8}
+
+
+def threshold_rule(rule: str, c: int, d: int, n: int, params=(), L: float = 0.0, M: float = 0.0, S: float = 0.0,
+                   hw: float = 1.0) -> float:
+    """Table 1 rows Feng / Rais / Khurshid / Phansalkar, canonical fp64."""
+    prm = np.ascontiguousarray(list(params) + [0.0] * (8 - len(params)), dtype=np.float64)
+    return _load().orc_threshold_rule(RULES[rule], c, d, n, prm.ctypes.data, L, M, S, hw)
+
+
+def global_mean_std(I):
+    I = _img(I)
+    M, S = ctypes.c_double(), ctypes.c_double()
+    _load().orc_global_mean_std(I.ctypes.data, I.shape[0], I.shape[1], I.strides[0], ctypes.byref(M), ctypes.byref(S))
+    return M.value, S.value
+
+
+def binarize_rule(rule: str, I, h: int, w: int, params=(), rows=None, cols=None, with_t: bool = False):
+    """Mask (and t) of a Table 1 rule on the whole page, or at sampled pixels."""
+    I = _img(I)
+    H, W = I.shape
+    prm = np.ascontiguousarray(list(params) + [0.0] * (8 - len(params)), dtype=np.float64)
+    if rows is None:
+        m, rp, cp = H * W, None, None
+        shape = (H, W)
+    else:
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        cols = np.ascontiguousarray(cols, dtype=np.int64)
+        m, rp, cp = rows.size, rows.ctypes.data, cols.ctypes.data
+        shape = (rows.size,)
+    mask = np.empty(shape, np.uint8)
+    t = np.empty(shape, np.float64)
+    _load().orc_binarize_rule(RULES[rule], I.ctypes.data, H, W, I.strides[0], h, w, prm.ctypes.data, m, rp, cp,
+                              mask.ctypes.data, t.ctypes.data)
+    return (mask, t) if with_t else mask
 
 
 def pack_bits(mask: np.ndarray) -> np.ndarray:

@@ -394,3 +394,95 @@ int orc_bernsen_points(const uint8_t *I, int64_t H, int64_t W, int64_t pitch, in
   return 0;
 }
 
+/* ---- The remaining Table 1 rows, "implemented by changing
+ * a single condition in Algorithm 1".  Each is the row
+ * written left to right in IEEE double (no contraction), after the canonical
+ * m = c/n, v = d/n - m^2 (clamped at 0), s = sqrt(v) of orc_threshold:
+ *   Feng       t = a1 m + k1 (s/R)^(1+g) (m - L) + k2 (s/R)^g L
+ *              params {a1, k1, k2, g, R}; L = global minimum
+ *   Rais       t = m + 0.3 (m s - M S) / max{m s, M S} s
+ *              M, S = global mean and standard deviation;
+ *              reading: 0/0 (both products zero) -> fraction 0 (R16)
+ *   Khurshid   t = m + k sqrt(s^2 + m^2 (N - 1) / N)
+ *              params {k, N_mode}: N = h w (the table's "hw") or, N_mode = 1,
+ *              the clamped count n (R17)
+ *   Phansalkar t = m (1 + p e^(-q m) + k (s/R - 1))
+ *              params {k, R, p, q}
+ */
+#define ORC_FENG 5
+#define ORC_RAIS 6
+#define ORC_KHURSHID 7
+#define ORC_PHANSALKAR 8
+
+double orc_threshold_rule(int32_t rule, uint64_t c, uint64_t d, uint64_t n, const double *prm, double L, double M,
+                          double S, double hw) {
+  double m = (double)c / (double)n;
+  double v = (double)d / (double)n - m * m;
+  if (v < 0) v = 0;
+  double s = sqrt(v);
+  switch (rule) {
+    case ORC_FENG: {
+      const double a1 = prm[0], k1 = prm[1], k2 = prm[2], g = prm[3], R = prm[4];
+      return a1 * m + k1 * pow(s / R, 1.0 + g) * (m - L) + k2 * pow(s / R, g) * L;
+    }
+    case ORC_RAIS: {
+      const double a = m * s, b = M * S;
+      const double den = a > b ? a : b;
+      const double frac = den > 0 ? (a - b) / den : 0.0;
+      return m + 0.3 * frac * s;
+    }
+    case ORC_KHURSHID: {
+      const double k = prm[0];
+      const double N = prm[1] != 0.0 ? (double)n : hw;
+      return m + k * sqrt(s * s + m * m * ((N - 1.0) / N));
+    }
+    case ORC_PHANSALKAR: {
+      const double k = prm[0], R = prm[1], p = prm[2], q = prm[3];
+      return m * (1.0 + p * exp(-q * m) + k * (s / R - 1.0));
+    }
+  }
+  return NAN;
+}
+
+/* Global mean M and standard deviation S of the gray levels (Table 1
+ * notation): exact integer sums, then M = sum/N,
+ * S = sqrt(sumsq/N - M^2) (clamped at 0). */
+void orc_global_mean_std(const uint8_t *I, int64_t H, int64_t W, int64_t pitch, double *M, double *S) {
+  uint64_t s1 = 0, s2 = 0;
+  for (int64_t i = 0; i < H; ++i)
+    for (int64_t j = 0; j < W; ++j) {
+      const uint64_t x = I[i * pitch + j];
+      s1 += x;
+      s2 += x * x;
+    }
+  const double N = (double)H * (double)W;
+  const double m = (double)s1 / N;
+  double v = (double)s2 / N - m * m;
+  if (v < 0) v = 0;
+  *M = m;
+  *S = sqrt(v);
+}
+
+/* Binarization by a Table 1 rule at the whole page (rows = NULL) or at m
+ * sampled pixels; t_out optional.  mask = 0 iff I <= t. */
+int orc_binarize_rule(int32_t rule, const uint8_t *I, int64_t H, int64_t W, int64_t pitch, int32_t h, int32_t w,
+                      const double *prm, int64_t m, const int64_t *rows, const int64_t *cols, uint8_t *mask,
+                      double *t_out) {
+  double L = 0, M = 0, S = 0;
+  if (rule == ORC_FENG) L = (double)orc_global_min(I, H, W, pitch);
+  if (rule == ORC_RAIS) orc_global_mean_std(I, H, W, pitch, &M, &S);
+  const double hw = (double)h * (double)w;
+  const int64_t total = rows ? m : H * W;
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t q = 0; q < total; ++q) {
+    const int64_t i = rows ? rows[q] : q / W, j = rows ? cols[q] : q % W;
+    uint64_t c, d;
+    direct_sums(I, H, W, pitch, h, w, i, j, &c, &d);
+    const uint64_t n = (uint64_t)orc_count(H, W, h, w, i, j);
+    const double t = orc_threshold_rule(rule, c, d, n, prm, L, M, S, hw);
+    mask[q] = ((double)I[i * pitch + j] <= t) ? 0 : 1;
+    if (t_out) t_out[q] = t;
+  }
+  return 0;
+}
+

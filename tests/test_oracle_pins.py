@@ -391,3 +391,83 @@ def test_bernsen_closed_forms():
     m, lo, hi = oracle.bernsen(J, 2 * 10 + 1, 2 * 12 + 1)
     assert (lo == J.min()).all() and (hi == J.max()).all()
     assert np.array_equal(m, (2 * J.astype(int) > int(J.min()) + int(J.max())).astype(np.uint8))
+
+
+# ------------------------------------------------ Table 1 rows Feng / Rais / Khurshid / Phansalkar
+
+def _stats_grid(seed=21, n=400):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        nn = int(rng.integers(1, 4000))
+        xs = rng.integers(0, 256, size=min(nn, 64))
+        c = int(xs.sum()) * nn // len(xs)
+        d = int((xs.astype(np.int64) ** 2).sum()) * nn // len(xs)
+        d = max(d, -(-c * c // nn))  # keep n d >= c^2 (a realisable window)
+        out.append((c, d, nn))
+    return out
+
+
+def test_rules_reduce_to_the_mean_threshold():
+    # k = 0 (and p = 0 / k1 = k2 = 0, a1 = 1) leaves t = m: the mean rule,
+    # i.e. Niblack with k = 0 from the other oracle function
+    for c, d, n in _stats_grid():
+        m = oracle.threshold("niblack", c, d, n, 0.0)
+        assert oracle.threshold_rule("khurshid", c, d, n, (0.0, 0), hw=9.0) == m
+        assert oracle.threshold_rule("phansalkar", c, d, n, (0.0, 128.0, 0.0, 3.0)) == m
+        assert abs(oracle.threshold_rule("feng", c, d, n, (1.0, 0.0, 0.0, 2.0, 128.0), L=7.0) - m) <= 1e-12 * max(1, m)
+
+
+def test_phansalkar_reduces_to_sauvola():
+    # p = 0: m (1 + k (s/R - 1)) -- Sauvola, evaluated by the other function
+    for c, d, n in _stats_grid(22):
+        assert oracle.threshold_rule("phansalkar", c, d, n, (0.3, 128.0, 0.0, 10.0)) == \
+            oracle.threshold("sauvola", c, d, n, 0.3, 128.0)
+        # q = 0: e^0 = 1, so t = Sauvola + p m
+        ts = oracle.threshold("sauvola", c, d, n, 0.3, 128.0)
+        tp = oracle.threshold_rule("phansalkar", c, d, n, (0.3, 128.0, 2.0, 0.0))
+        assert abs(tp - (ts + 2.0 * c / n)) <= 1e-9 * max(1.0, abs(tp))
+
+
+def test_feng_with_gamma_zero_is_wolf():
+    # gamma = 0, a1 = 1 - k, k1 = k2 = k:
+    #   (1-k) m + k (s/R)(m - L) + k L  =  m - k (m - L)(1 - s/R)   (Wolf)
+    for c, d, n in _stats_grid(23):
+        for L in (0.0, 17.0):
+            tw = oracle.threshold("wolf", c, d, n, 0.5, 128.0, L)
+            tf = oracle.threshold_rule("feng", c, d, n, (0.5, 0.5, 0.5, 0.0, 128.0), L=L)
+            assert abs(tw - tf) <= 1e-9 * max(1.0, abs(tw))
+
+
+def test_khurshid_with_N_one_is_niblack():
+    # N = 1 removes the m^2 term: m + k sqrt(s^2) = Niblack
+    for c, d, n in _stats_grid(24):
+        tn = oracle.threshold("niblack", c, d, n, -0.2)
+        tk = oracle.threshold_rule("khurshid", c, d, n, (-0.2, 0), hw=1.0)
+        assert abs(tn - tk) <= 1e-12 * max(1.0, abs(tn))
+
+
+def test_rais_closed_forms():
+    # constant image: s = S = 0, 0/0 -> fraction 0 (R16) -> t = m = g
+    g = synth.constant(20, 30, 140)
+    mask, t = oracle.binarize_rule("rais", g, 5, 5, (), with_t=True)
+    assert (t == 140.0).all() and (mask == 0).all()
+    # whole-image window: every pixel sees m = M and s = S -> fraction 0 ->
+    # the global mean threshold
+    I = synth.uniform_random(18, 23, 31)
+    M, S = oracle.global_mean_std(I)
+    assert abs(M - I.mean()) < 1e-12 and abs(S - I.std()) < 1e-9
+    mask, t = oracle.binarize_rule("rais", I, 2 * 18 + 1, 2 * 23 + 1, (), with_t=True)
+    assert (t == M).all()
+    assert np.array_equal(mask, (I > M).astype(np.uint8))
+
+
+def test_rule_points_equal_full_page():
+    I = synth.page(40, 70, synth.config_seed(3, 9), stain=True)
+    rows = np.repeat(np.arange(40), 70)
+    cols = np.tile(np.arange(70), 40)
+    for rule, prm in [("feng", (0.15, 0.2, 0.03, 2.0, 128.0)), ("rais", ()), ("khurshid", (0.2, 1)),
+                      ("phansalkar", (0.25, 128.0, 3.0, 10.0 / 255.0))]:
+        full = oracle.binarize_rule(rule, I, 9, 11, prm)
+        pts = oracle.binarize_rule(rule, I, 9, 11, prm, rows=rows, cols=cols)
+        assert np.array_equal(full.ravel(), pts), rule
