@@ -130,6 +130,22 @@ int abin_quantile(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uin
 int abin_bernsen(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out, int64_t out_pitch,
                  int32_t mask_format, int32_t h, int32_t w, int32_t contrast, uint32_t flags, void* stream);
 
+/* ---- The remaining Table 1 rows ---------------------------
+ * rule and params (host array, n_params >= the count below):
+ *   ABIN_FENG        {a1, k1, k2, gamma, R}: t = a1 m + k1 (s/R)^(1+gamma) (m - L) + k2 (s/R)^gamma L,
+ *                    L = the page's global minimum (computed on the device)
+ *   ABIN_RAIS        {}: t = m + 0.3 (m s - M S) / max{m s, M S} s, M / S = the page's global mean /
+ *                    standard deviation (computed on the device); 0/0 -> 0
+ *   ABIN_KHURSHID    {k, N_mode}: t = m + k sqrt(s^2 + m^2 (N - 1)/N), N = h w (N_mode = 0) or the
+ *                    clamped count n (N_mode != 0)
+ *   ABIN_PHANSALKAR  {k, R, p, q}: t = m (1 + p e^(-q m) + k (s/R - 1))
+ * Every pixel is decided in IEEE double (left-to-right evaluation; pow/exp are
+ * the device's double routines, <= 2 ulp).  ABIN_EINVAL for an unknown rule,
+ * missing or non-finite params, R <= 0. */
+int abin_binarize_rule(int32_t rule, const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out,
+                       int64_t out_pitch, int32_t mask_format, int32_t h, int32_t w, const double* params,
+                       int32_t n_params, uint32_t flags, uint64_t* counters, void* stream);
+
 /* ---- Page batches ------------------------------------------------------------
  * n_pages pages of identical H x W geometry; page p is read at
  * in + p * in_page_stride and written at out + p * out_page_stride (bytes).
@@ -138,6 +154,7 @@ int abin_bernsen(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint
  * param0 = k (or q, contrast), param1 = R.
  * With ABIN_HOST_IO, in/out are host pointers. */
 enum { ABIN_SAUVOLA = 0, ABIN_NIBLACK = 1, ABIN_WOLF = 2, ABIN_QUANTILE = 3, ABIN_BERNSEN = 4 };
+enum { ABIN_FENG = 5, ABIN_RAIS = 6, ABIN_KHURSHID = 7, ABIN_PHANSALKAR = 8 };
 int abin_binarize_batched(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8_t* out,
                           int64_t out_page_stride, int64_t n_pages, int64_t H, int64_t W, int64_t in_pitch,
                           int64_t out_pitch, int32_t mask_format, int32_t h, int32_t w, double param0,

@@ -37,6 +37,8 @@ _lib.abin_niblack.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, 
 _lib.abin_wolf.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _D, _D, _I32, _U32, _P, _P]
 _lib.abin_quantile.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _D, _U32, _P]
 _lib.abin_bernsen.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _I32, _U32, _P]
+_lib.abin_binarize_rule.argtypes = [_I32, _P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _P, _I32, _U32, _P, _P]
+RULES = {"feng": 5, "rais": 6, "khurshid": 7, "phansalkar": 8}
 _lib.abin_binarize_batched.argtypes = [_I32, _P, _I64, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _D,
                                        _D, _I32, _U32, _P, _P]
 _lib.abin_binarize_band.argtypes = [_I32, _P, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _P, _I64, _I32, _I32, _I32,
@@ -55,7 +57,8 @@ class AbinLimits(ctypes.Structure):
 
 _lib.abin_limits.argtypes = [ctypes.POINTER(AbinLimits)]
 
-EXPORTED = ["abin_sauvola", "abin_niblack", "abin_wolf", "abin_quantile", "abin_bernsen", "abin_binarize_batched",
+EXPORTED = ["abin_sauvola", "abin_niblack", "abin_wolf", "abin_quantile", "abin_bernsen", "abin_binarize_rule",
+            "abin_binarize_batched",
             "abin_binarize_band", "abin_global_min", "abin_stats", "abin_limits", "abin_strerror", "abin_version",
             "abin_last_cuda_error"]
 
@@ -156,6 +159,18 @@ def bernsen(img: torch.Tensor, h: int, w: int, contrast: int = -1, packed: bool 
     out = _alloc_mask(H, W, packed, img.device) if out is None else out
     _check(_lib.abin_bernsen(_ptr(img), H, W, pitch, _ptr(out), out.stride(0), MASK_BITS if packed else MASK_U8, h,
                              w, contrast, flags, _stream(stream)))
+    return out
+
+
+def binarize_rule(rule: str, img: torch.Tensor, h: int, w: int, params=(), packed: bool = False, out=None,
+                  flags: int = 0, counters: torch.Tensor = None, stream=None) -> torch.Tensor:
+    """Feng / Rais / Khurshid / Phansalkar (Table 1); params as in abin.h."""
+    H, W, pitch = _img2d(img)
+    out = _alloc_mask(H, W, packed, img.device) if out is None else out
+    prm = (ctypes.c_double * max(1, len(params)))(*params)
+    _check(_lib.abin_binarize_rule(RULES[rule], _ptr(img), H, W, pitch, _ptr(out), out.stride(0),
+                                   MASK_BITS if packed else MASK_U8, h, w, prm, len(params), flags, _ptr(counters),
+                                   _stream(stream)))
     return out
 
 

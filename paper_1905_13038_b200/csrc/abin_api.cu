@@ -205,6 +205,8 @@ struct MomCall {
   uint32_t* n_out;
   double* t_out;
   uint8_t* mask_out;
+  // Table 1 rules (methods 5..8): parameters, see abin.h
+  double rprm[5];
 };
 
 // Row bands: pick the band count so that the tile count fills whole waves
@@ -303,7 +305,8 @@ int run_moments(const MomCall& c) {
   // generic loader stages the rows.
   const bool tma_ok = !((reinterpret_cast<uintptr_t>(c.in) & 15u) || (c.in_pitch & 15) ||
                         (c.n_pages > 1 && (c.in_page_stride & 15))) && !(c.flags & ABIN_NO_TMA_INTERNAL);
-  const bool use_v4 = fast && tma_ok && !(c.flags & ABIN_V3_INTERNAL);
+  const bool rule = c.method >= ABIN_FENG && c.method <= ABIN_PHANSALKAR;
+  const bool use_v4 = fast && tma_ok && !(c.flags & ABIN_V3_INTERNAL) && !rule;
   CUtensorMap map;
   int rc = use_v4 ? encode_map_chunks(c, v4::kChunks, v4::kR, &map)
                   : encode_map(c, fast ? kR : (nt_wide == 128 ? 8 : 4), tma_ok, &map);
@@ -311,7 +314,7 @@ int run_moments(const MomCall& c) {
 
   unsigned int* Lw = nullptr;
   const uint8_t* L8 = nullptr;
-  if (c.method == M_WOLF && c.L_override < 0) {
+  if ((c.method == M_WOLF || c.method == ABIN_FENG) && c.L_override < 0) {
     CK(cudaMallocAsync(&Lw, (size_t)c.n_pages * 4 + (size_t)c.n_pages, c.stream));
     uint8_t* l8 = reinterpret_cast<uint8_t*>(Lw + c.n_pages);
     k_fill_u32<<<(unsigned)((c.n_pages + 255) / 256), 256, 0, c.stream>>>(Lw, c.n_pages, 0xFFu);
@@ -321,6 +324,23 @@ int run_moments(const MomCall& c) {
     k_narrow_u8<<<(unsigned)((c.n_pages + 255) / 256), 256, 0, c.stream>>>(Lw, l8, c.n_pages);
     CK(cudaGetLastError());
     L8 = l8;
+  }
+  // Rais: per-page global mean / standard deviation M, S
+  unsigned long long* acc = nullptr;
+  RuleParams rp;
+  memset(&rp, 0, sizeof(rp));
+  for (int z = 0; z < 5; ++z) rp.p[z] = c.rprm[z];
+  rp.hw = (double)c.h * (double)c.w;
+  if (c.method == ABIN_RAIS) {
+    CK(cudaMallocAsync(&acc, (size_t)c.n_pages * 32, c.stream));
+    CK(cudaMemsetAsync(acc, 0, (size_t)c.n_pages * 16, c.stream));
+    double* MS = reinterpret_cast<double*>(acc + 2 * c.n_pages);
+    k_global_sums<<<dim3(148, (unsigned)c.n_pages), 256, 0, c.stream>>>(c.in, c.in_page_stride, c.H_out, c.W,
+                                                                          c.in_pitch, acc);
+    k_mean_std<<<(unsigned)((c.n_pages + 127) / 128), 128, 0, c.stream>>>(acc, MS, c.n_pages,
+                                                                            (double)c.H_out * (double)c.W);
+    CK(cudaGetLastError());
+    rp.MS = MS;
   }
   const bool d64 = (c.flags & ABIN_FORCE_U64_SQ) || (uint64_t)win.h * (uint64_t)win.w * 65025u >= (1ull << 32);
   const int ph = ((-win.w) % 4 + 4) % 4;
@@ -340,7 +360,8 @@ int run_moments(const MomCall& c) {
     p.n_strips = (int32_t)((c.W + (int64_t)kCW * p.Tw - 1) / ((int64_t)kCW * p.Tw));
     choose_bands((int64_t)p.n_strips * c.n_pages, c.H_out, win.h, 148 * 4, &p.B, &p.n_bands);
     p.method = c.method;
-    p.force_fp64 = (c.flags & ABIN_FORCE_FP64) ? 1 : 0;
+    p.force_fp64 = ((c.flags & ABIN_FORCE_FP64) || rule) ? 1 : 0;  // rules: every pixel in IEEE double
+    p.rp = rp;
     p.k = c.k; p.R = c.R;
     p.L_page = L8; p.L_fixed = c.L_override;
     const FilterConsts f = filter_consts(c.method, c.k, c.R);
@@ -390,6 +411,7 @@ int run_moments(const MomCall& c) {
     choose_bands((int64_t)p.n_strips * c.n_pages, c.H_out, win.h, 148 * 2, &p.B, &p.n_bands);
     p.method = c.method;
     p.force_fp64 = 1;
+    p.rp = rp;
     p.out_vec_ok = ((reinterpret_cast<uintptr_t>(c.out) | (uintptr_t)c.out_pitch |
                      (uintptr_t)(c.n_pages > 1 ? c.out_page_stride : 0)) & 7u) == 0;
     p.k = c.k; p.R = c.R;
@@ -403,6 +425,10 @@ int run_moments(const MomCall& c) {
     cudaError_t e = cudaFreeAsync(Lw, c.stream);
     if (rc == ABIN_OK && e != cudaSuccess) return cuda_fail(e);
   }
+  if (acc) {
+    cudaError_t e = cudaFreeAsync(acc, c.stream);
+    if (rc == ABIN_OK && e != cudaSuccess) return cuda_fail(e);
+  }
   return rc;
 }
 
@@ -412,7 +438,7 @@ int check_params(int32_t method, double p0, double p1) {
   if (!std::isfinite(p0)) return ABIN_EINVAL;
   if (method == ABIN_SAUVOLA || method == ABIN_WOLF)
     if (!std::isfinite(p1) || !(p1 > 0.0)) return ABIN_EINVAL;
-  if (method < 0 || method > 4) return ABIN_EINVAL;
+  if (method < 0 || method > 8) return ABIN_EINVAL;
   return ABIN_OK;
 }
 
@@ -658,6 +684,46 @@ int abin_quantile(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uin
                   int32_t mask_format, int32_t h, int32_t w, double q, uint32_t flags, void* stream) {
   return abin_binarize_batched(ABIN_QUANTILE, in, 0, out, 0, 1, H, W, in_pitch, out_pitch, mask_format, h, w, q,
                                0.0, -1, flags, nullptr, stream);
+}
+
+int abin_binarize_rule(int32_t rule, const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out,
+                       int64_t out_pitch, int32_t mask_format, int32_t h, int32_t w, const double* params,
+                       int32_t n_params, uint32_t flags, uint64_t* counters, void* stream) {
+  int rc = check_common(in, H, W, in_pitch, out, out_pitch, mask_format, h, w);
+  if (rc) return rc;
+  static const int need[4] = {5, 0, 2, 4};  // Feng, Rais, Khurshid, Phansalkar
+  if (rule < ABIN_FENG || rule > ABIN_PHANSALKAR) return ABIN_EINVAL;
+  const int k = need[rule - ABIN_FENG];
+  if (n_params < k || (k > 0 && !params)) return ABIN_EINVAL;
+  for (int z = 0; z < k; ++z)
+    if (!std::isfinite(params[z])) return ABIN_EINVAL;
+  if (rule == ABIN_FENG && !(params[4] > 0.0)) return ABIN_EINVAL;        // R
+  if (rule == ABIN_PHANSALKAR && !(params[1] > 0.0)) return ABIN_EINVAL;  // R
+  const int64_t out_row = mask_format == ABIN_MASK_U8 ? W : (W + 7) / 8;
+  if (overlaps(in, (size_t)((H - 1) * in_pitch + W), out, (size_t)((H - 1) * out_pitch + out_row))) return ABIN_EALIAS;
+  MomCall c;
+  memset(&c, 0, sizeof(c));
+  c.method = rule;
+  c.in = in;
+  c.buf_rows = H;
+  c.n_pages = 1;
+  c.W = W;
+  c.in_pitch = in_pitch;
+  c.H_out = H;
+  c.H_global = H;
+  c.out = out;
+  c.out_pitch = out_pitch;
+  c.fmt = mask_format;
+  c.h = h;
+  c.w = w;
+  c.k = 0.0;
+  c.R = 128.0;
+  c.L_override = -1;
+  c.flags = flags;
+  c.counters = counters;
+  c.stream = reinterpret_cast<cudaStream_t>(stream);
+  for (int z = 0; z < k; ++z) c.rprm[z] = params[z];
+  return run_moments(c);
 }
 
 int abin_bernsen(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out, int64_t out_pitch,

@@ -31,6 +31,7 @@
 #include <type_traits>
 
 #include "ptx.cuh"
+#include "rules.cuh"
 
 namespace abin {
 
@@ -66,6 +67,7 @@ struct MomParams {
   uint64_t* counters;        // [near_tie, fp64 fallbacks(, stage-2 pixels)] or null
   int32_t counters_n;        // 2, or 3 with ABIN_COUNT_STAGES
   int32_t sL, sR;            // v4: strips [sL, sR) are interior (no image border inside their windows)
+  RuleParams rp;             // Table 1 rules Feng / Rais / Khurshid / Phansalkar (rules.cuh)
   int32_t n_pages_v4;        // v4: pages of the launch
   // statistics mode (page 0 only)
   uint64_t* c_out;
@@ -446,7 +448,8 @@ __global__ void __launch_bounds__(kNT, 4) k_moments(const __grid_constant__ CUte
   int lofs[5];                                        // swizzled word offsets of the leaving chunks
 #pragma unroll
   for (int g = 0; g < 5; ++g) lofs[g] = swz(min(st0 + 4 * g, kWarpRow - 4));
-  const float Lf = (p.method == M_WOLF) ? (float)(p.L_fixed >= 0 ? p.L_fixed : (int)p.L_page[page]) : 0.0f;
+  const float Lf = (p.method == M_WOLF || p.method == M_FENG)
+                       ? (float)(p.L_fixed >= 0 ? p.L_fixed : (int)p.L_page[page]) : 0.0f;
   const bool slow_all = p.stats || p.force_fp64;
   const int method = p.method;
   const float delta1 = p.delta1;
@@ -632,7 +635,8 @@ __global__ void __launch_bounds__(kNT, 4) k_moments(const __grid_constant__ CUte
           }
           double tt = 0.0;
           if (!decided) {
-            tt = threshold_fp64(p.method, c64, d64, n, p.k, p.R, (double)Lf);
+            tt = is_rule(p.method) ? threshold_rule_fp64(p.method, c64, d64, n, p.rp, (double)Lf, page)
+                                   : threshold_fp64(p.method, c64, d64, n, p.k, p.R, (double)Lf);
             mk = ((double)I <= tt) ? 0u : 1u;
             fallbacks++;
             if (fabs((double)I - tt) < 1e-9) near_ties++;

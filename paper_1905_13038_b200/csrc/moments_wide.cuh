@@ -29,6 +29,7 @@
 #include <type_traits>
 
 #include "ptx.cuh"
+#include "rules.cuh"
 
 namespace abin {
 namespace wide {
@@ -70,6 +71,7 @@ struct MomParams {
   int32_t use_tma;
   const uint8_t* in;
   int64_t in_pitch, in_page_stride, buf_rows;
+  RuleParams rp;  // Table 1 rules Feng / Rais / Khurshid / Phansalkar (rules.cuh)
 };
 
 // ------------------------------------------------------------------ epilogue
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(NT) k_moments(const __grid_constant__ CUtensor
     const int64_t j = j0 + t;
     ncol[t] = (int)(min(j + p.r, p.W - 1) - max(j - p.l, (int64_t)-1));
   }
-  const double Lw = (p.method == M_WOLF) ? (double)(p.L_fixed >= 0 ? p.L_fixed : (int)p.L_page[page]) : 0.0;
+  const double Lw = (p.method == M_WOLF || p.method == M_FENG) ? (double)(p.L_fixed >= 0 ? p.L_fixed : (int)p.L_page[page]) : 0.0;
 
   uint32_t C[G], D[G];
 #pragma unroll
@@ -404,7 +406,8 @@ __global__ void __launch_bounds__(NT) k_moments(const __grid_constant__ CUtensor
         cc += C[t] - Cl[t];
         dd += (DT)D[t] - (DT)Dl[t];
         const uint32_t n = (uint32_t)(ncol[t] * nrow);
-        const double tt = threshold_fp64(p.method, (uint64_t)cc, (uint64_t)dd, n, p.k, p.R, Lw);
+        const double tt = is_rule(p.method) ? threshold_rule_fp64(p.method, (uint64_t)cc, (uint64_t)dd, n, p.rp, Lw, page)
+                                            : threshold_fp64(p.method, (uint64_t)cc, (uint64_t)dd, n, p.k, p.R, Lw);
         const double I = (double)xc.at(t);
         const uint32_t mk = (I <= tt) ? 0u : 1u;
         mbits |= mk << t;

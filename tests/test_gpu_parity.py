@@ -328,3 +328,44 @@ def test_bernsen_constant_and_bands():
     mb = ab.binarize_batched("bernsen", torch.from_numpy(P).to(DEV), 15, 15, -1.0).cpu().numpy()
     for p in range(3):
         assert np.array_equal(mb[p], oracle.bernsen(P[p], 15, 15)[0])
+
+
+# ------------------------------------------------ Table 1 rules (NEXT #2)
+
+RULE_PARAMS = {"feng": (0.85, 0.2, 0.05, 2.0, 64.0), "rais": (), "khurshid": (-0.1, 0),
+               "phansalkar": (0.25, 128.0, 3.0, 10.0 / 255.0)}
+
+
+@pytest.mark.parametrize("rule", sorted(RULE_PARAMS))
+def test_table1_rules(rule):
+    """Feng / Rais / Khurshid / Phansalkar (PAPER.md:154-157) decided in IEEE
+    double on the GPU vs the oracle.  Rais and Khurshid use only IEEE-exact
+    operations: masks bit-exact.  Feng and Phansalkar call pow / exp (device
+    <= 2 ulp vs glibc): masks bit-exact except pixels within 1e-9 of the
+    oracle's threshold (R18)."""
+    prm = RULE_PARAMS[rule]
+    cases = [((300, 700), (61, 61), None), ((257, 333), (32, 17), 333), ((90, 1200), (15, 600), None),
+             ((64, 64), (1, 1), None)]
+    for (H, W), (h, w), pitch in cases:
+        I = synth.page(H, W, synth.config_seed(3, H), stain=True)
+        ref, t = oracle.binarize_rule(rule, I, h, w, prm, with_t=True)
+        got = ab.binarize_rule(rule, to_dev(I, pitch), h, w, prm).cpu().numpy()
+        tie = np.abs(I.astype(np.float64) - t) < 1e-9
+        if rule in ("rais", "khurshid"):
+            assert np.array_equal(got, ref), (rule, H, W, int((got != ref).sum()))
+        else:  # any mismatch must sit on a near tie (pow / exp last-ulp differences)
+            assert not ((got != ref) & ~tie).any(), (rule, H, W)
+        gb = ab.binarize_rule(rule, to_dev(I, pitch), h, w, prm, packed=True).cpu().numpy()
+        assert np.array_equal(gb, oracle.pack_bits(got))
+    if rule == "khurshid":  # N = n variant
+        I = synth.page(120, 200, synth.config_seed(3, 7))
+        assert np.array_equal(ab.binarize_rule(rule, to_dev(I), 9, 9, (-0.1, 1)).cpu().numpy(),
+                              oracle.binarize_rule(rule, I, 9, 9, (-0.1, 1)))
+
+
+def test_table1_rules_validation():
+    x = torch.zeros((8, 8), dtype=torch.uint8, device=DEV)
+    with pytest.raises(abin.AbinError):
+        ab.binarize_rule("feng", x, 3, 3, (0.5, 0.2, 0.05))          # too few params
+    with pytest.raises(abin.AbinError):
+        ab.binarize_rule("phansalkar", x, 3, 3, (0.25, 0.0, 3.0, 0.1))  # R <= 0
