@@ -67,6 +67,8 @@ def _load():
         lib.orc_threshold_rule.restype = _D
         lib.orc_global_mean_std.argtypes = [_P, _I64, _I64, _I64, _P, _P]
         lib.orc_binarize_rule.argtypes = [_I32, _P, _I64, _I64, _I64, _I32, _I32, _P, _I64, _P, _P, _P, _P]
+        lib.orc_otsu.argtypes = [_P, _I64, _I64, _I64]
+        lib.orc_otsu.restype = _I32
         lib.orc_num_threads.restype = ctypes.c_int
         lib.orc_set_threads.argtypes = [ctypes.c_int]
         _lib = lib
@@ -258,6 +260,13 @@ def binarize_rule(rule: str, I, h: int, w: int, params=(), rows=None, cols=None,
     _load().orc_binarize_rule(RULES[rule], I.ctypes.data, H, W, I.strides[0], h, w, prm.ctypes.data, m, rp, cp,
                               mask.ctypes.data, t.ctypes.data)
     return (mask, t) if with_t else mask
+
+
+def otsu(I):
+    """Otsu's global threshold t and the mask (0 iff I <= t)."""
+    I = _img(I)
+    t = int(_load().orc_otsu(I.ctypes.data, I.shape[0], I.shape[1], I.strides[0]))
+    return t, (I > t).astype(np.uint8)
 
 
 def pack_bits(mask: np.ndarray) -> np.ndarray:

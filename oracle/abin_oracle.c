@@ -486,3 +486,43 @@ int orc_binarize_rule(int32_t rule, const uint8_t *I, int64_t H, int64_t W, int6
   return 0;
 }
 
+/* ---- Otsu's global threshold (the paper's speed
+ * comparator; SPEC threshold-rules otsu_threshold) -------------------------
+ * Histogram h(g) of the page (exact counts), then the t in 0..255 maximising
+ * the between-class variance  sigma_b^2(t) = w0 w1 (mu0 - mu1)^2  with
+ * w0 = N0/N, w1 = N1/N (N0 = #(x <= t), N1 = N - N0) and mu0, mu1 the class
+ * means; classes with no pixels give sigma_b^2 = 0; ties keep the smallest t.
+ * Evaluated in IEEE double in this order:
+ *   w0 = N0/N, w1 = N1/N, mu0 = S0/N0, mu1 = S1/N1, d = mu0 - mu1,
+ *   sb = (w0 * w1) * (d * d)
+ * (S0 = sum of g h(g) over g <= t).  Foreground iff I <= t. */
+int32_t orc_otsu(const uint8_t *I, int64_t H, int64_t W, int64_t pitch) {
+  uint64_t hist[256] = {0};
+  for (int64_t i = 0; i < H; ++i)
+    for (int64_t j = 0; j < W; ++j) hist[I[i * pitch + j]]++;
+  const uint64_t N = (uint64_t)H * (uint64_t)W;
+  uint64_t Stot = 0;
+  for (int g = 0; g < 256; ++g) Stot += (uint64_t)g * hist[g];
+  const double Nd = (double)N;
+  uint64_t N0 = 0, S0 = 0;
+  double best = -1.0;
+  int32_t tbest = 0;
+  for (int t = 0; t < 256; ++t) {
+    N0 += hist[t];
+    S0 += (uint64_t)t * hist[t];
+    const uint64_t N1 = N - N0, S1 = Stot - S0;
+    double sb = 0.0;
+    if (N0 > 0 && N1 > 0) {
+      const double w0 = (double)N0 / Nd, w1 = (double)N1 / Nd;
+      const double mu0 = (double)S0 / (double)N0, mu1 = (double)S1 / (double)N1;
+      const double d = mu0 - mu1;
+      sb = (w0 * w1) * (d * d);
+    }
+    if (sb > best) {
+      best = sb;
+      tbest = t;
+    }
+  }
+  return tbest;
+}
+

@@ -471,3 +471,38 @@ def test_rule_points_equal_full_page():
         full = oracle.binarize_rule(rule, I, 9, 11, prm)
         pts = oracle.binarize_rule(rule, I, 9, 11, prm, rows=rows, cols=cols)
         assert np.array_equal(full.ravel(), pts), rule
+
+
+# ---------------------------------------------------------------- Otsu
+
+def test_otsu_two_levels_separates_perfectly():
+    I = np.full((30, 40), 200, np.uint8)
+    I[5:17, 3:30] = 40
+    t, mask = oracle.otsu(I)
+    assert t == 40                       # every t in [40, 200) is optimal; the smallest is kept
+    assert np.array_equal(mask, (I == 200).astype(np.uint8))
+
+
+def test_otsu_minimises_within_class_variance():
+    # Otsu's equivalence: maximising sigma_b^2 = minimising the weighted
+    # within-class variance w0 var0 + w1 var1, computed here directly from
+    # the pixel subsets (a different quantity from the oracle's)
+    for seed in (1, 2, 3):
+        I = synth.page(60, 90, synth.config_seed(9, seed), stain=bool(seed & 1))
+        t, _ = oracle.otsu(I)
+        x = I.ravel().astype(np.float64)
+        def within(tt):
+            a, b = x[x <= tt], x[x > tt]
+            if a.size == 0 or b.size == 0:
+                return np.inf
+            return (a.size * a.var() + b.size * b.var()) / x.size
+        wv = np.array([within(tt) for tt in range(256)])
+        assert within(t) <= wv.min() * (1 + 1e-12)
+
+
+def test_otsu_invariances():
+    I = synth.uniform_random(50, 60, 7, lo=20, hi=180)
+    t, _ = oracle.otsu(I)
+    assert oracle.otsu((I + 30).astype(np.uint8))[0] == t + 30                 # shift equivariance
+    rng = np.random.default_rng(3)
+    assert oracle.otsu(rng.permutation(I.ravel()).reshape(60, 50))[0] == t    # only the histogram matters
