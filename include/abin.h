@@ -146,6 +146,13 @@ int abin_binarize_rule(int32_t rule, const uint8_t* in, int64_t H, int64_t W, in
                        int64_t out_pitch, int32_t mask_format, int32_t h, int32_t w, const double* params,
                        int32_t n_params, uint32_t flags, uint64_t* counters, void* stream);
 
+/* ---- Otsu's global threshold (the paper's speed comparator)
+ * t = the gray level maximising the between-class variance w0 w1 (mu0 - mu1)^2 of
+ * the page histogram (IEEE double, ties keep the smallest t); I' = 0 iff I <= t.
+ * t_out: optional device byte receiving t. */
+int abin_otsu(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out, int64_t out_pitch,
+              int32_t mask_format, uint8_t* t_out, uint32_t flags, void* stream);
+
 /* ---- Page batches ------------------------------------------------------------
  * n_pages pages of identical H x W geometry; page p is read at
  * in + p * in_page_stride and written at out + p * out_page_stride (bytes).

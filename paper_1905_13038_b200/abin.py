@@ -39,6 +39,7 @@ _lib.abin_quantile.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32,
 _lib.abin_bernsen.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _I32, _U32, _P]
 _lib.abin_binarize_rule.argtypes = [_I32, _P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _P, _I32, _U32, _P, _P]
 RULES = {"feng": 5, "rais": 6, "khurshid": 7, "phansalkar": 8}
+_lib.abin_otsu.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _P, _U32, _P]
 _lib.abin_binarize_batched.argtypes = [_I32, _P, _I64, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _D,
                                        _D, _I32, _U32, _P, _P]
 _lib.abin_binarize_band.argtypes = [_I32, _P, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _P, _I64, _I32, _I32, _I32,
@@ -57,7 +58,7 @@ class AbinLimits(ctypes.Structure):
 
 _lib.abin_limits.argtypes = [ctypes.POINTER(AbinLimits)]
 
-EXPORTED = ["abin_sauvola", "abin_niblack", "abin_wolf", "abin_quantile", "abin_bernsen", "abin_binarize_rule",
+EXPORTED = ["abin_sauvola", "abin_niblack", "abin_wolf", "abin_quantile", "abin_bernsen", "abin_binarize_rule", "abin_otsu",
             "abin_binarize_batched",
             "abin_binarize_band", "abin_global_min", "abin_stats", "abin_limits", "abin_strerror", "abin_version",
             "abin_last_cuda_error"]
@@ -172,6 +173,16 @@ def binarize_rule(rule: str, img: torch.Tensor, h: int, w: int, params=(), packe
                                    MASK_BITS if packed else MASK_U8, h, w, prm, len(params), flags, _ptr(counters),
                                    _stream(stream)))
     return out
+
+
+def otsu(img: torch.Tensor, packed: bool = False, out=None, t_out: torch.Tensor = None, stream=None):
+    """Otsu's global threshold: returns (mask, t) with t a device uint8 tensor."""
+    H, W, pitch = _img2d(img)
+    out = _alloc_mask(H, W, packed, img.device) if out is None else out
+    t = torch.empty(1, dtype=torch.uint8, device=img.device) if t_out is None else t_out
+    _check(_lib.abin_otsu(_ptr(img), H, W, pitch, _ptr(out), out.stride(0), MASK_BITS if packed else MASK_U8, _ptr(t),
+                          0, _stream(stream)))
+    return out, t
 
 
 def binarize_batched(method: str, pages: torch.Tensor, h: int, w: int, param0: float, param1: float = 128.0,

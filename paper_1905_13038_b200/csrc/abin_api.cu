@@ -13,6 +13,7 @@
 
 #include "../../include/abin.h"
 #include "globalmin.cuh"
+#include "otsu.cuh"
 #include "launch.cuh"
 #include "quantile.cuh"
 
@@ -724,6 +725,30 @@ int abin_binarize_rule(int32_t rule, const uint8_t* in, int64_t H, int64_t W, in
   c.stream = reinterpret_cast<cudaStream_t>(stream);
   for (int z = 0; z < k; ++z) c.rprm[z] = params[z];
   return run_moments(c);
+}
+
+int abin_otsu(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out, int64_t out_pitch,
+              int32_t mask_format, uint8_t* t_out, uint32_t flags, void* stream) {
+  (void)flags;
+  int rc = check_common(in, H, W, in_pitch, out, out_pitch, mask_format, 1, 1);
+  if (rc) return rc;
+  const int64_t out_row = mask_format == ABIN_MASK_U8 ? W : (W + 7) / 8;
+  if (overlaps(in, (size_t)((H - 1) * in_pitch + W), out, (size_t)((H - 1) * out_pitch + out_row))) return ABIN_EALIAS;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  unsigned long long* hist = nullptr;
+  CK(cudaMallocAsync(&hist, 256 * 8 + 16, st));
+  uint8_t* tdev = reinterpret_cast<uint8_t*>(hist + 256);
+  CK(cudaMemsetAsync(hist, 0, 256 * 8, st));
+  const unsigned nb = (unsigned)std::min<int64_t>(H, 4 * 148);
+  k_otsu_hist<<<dim3(nb, 1), 256, 0, st>>>(in, 0, H, W, in_pitch, hist);
+  k_otsu_pick<<<1, 32, 0, st>>>(hist, t_out ? t_out : tdev, 1, (double)H * (double)W);
+  k_otsu_mask<<<dim3(nb, 1), 256, 0, st>>>(in, 0, H, W, in_pitch, t_out ? t_out : tdev, out, out_pitch, 0,
+                                            mask_format);
+  cudaError_t e = cudaGetLastError();
+  cudaError_t f = cudaFreeAsync(hist, st);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (f != cudaSuccess) return cuda_fail(f);
+  return ABIN_OK;
 }
 
 int abin_bernsen(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out, int64_t out_pitch,

@@ -369,3 +369,20 @@ def test_table1_rules_validation():
         ab.binarize_rule("feng", x, 3, 3, (0.5, 0.2, 0.05))          # too few params
     with pytest.raises(abin.AbinError):
         ab.binarize_rule("phansalkar", x, 3, 3, (0.25, 0.0, 3.0, 0.1))  # R <= 0
+
+
+# ------------------------------------------------------------ Otsu (NEXT #4)
+
+def test_otsu_equals_oracle():
+    """Otsu's global threshold: the device histogram + the
+    IEEE-double scan in the oracle's order give the same t and mask."""
+    cases = [synth.page(300, 777, synth.config_seed(9, 1), stain=True), synth.uniform_random(129, 130, 4),
+             synth.constant(40, 50, 33), synth.page(7016, 4960, synth.config_seed(3), stain=True)]
+    for I in cases:
+        t, ref = oracle.otsu(I)
+        for pitch in (None, I.shape[1]):
+            m, tt = ab.otsu(to_dev(I, pitch))
+            assert int(tt.item()) == t
+            assert np.array_equal(m.cpu().numpy(), ref)
+        mb, _ = ab.otsu(to_dev(I), packed=True)
+        assert np.array_equal(mb.cpu().numpy(), oracle.pack_bits(ref))
