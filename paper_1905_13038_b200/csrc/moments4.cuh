@@ -385,6 +385,11 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
   constexpr int method = METHOD;
   // rows whose window is clipped by the top / bottom image edge: nrow < h
   const int64_t i_full0 = p.o - 1, i_full1 = p.H_global - 1 - p.u;  // nrow == h for i in [i_full0, i_full1]
+  // per-row scalars kept in registers (the compiler would otherwise re-load
+  // them from the parameter bank every row, exposing the load latency)
+  int64_t in_pitch = p.in_pitch, out_pitch = p.out_pitch;
+  uint32_t store_mode = !valid_lane ? 0u : (p.fmt != 0 ? 3u : (out_vec ? 1u : 2u));
+  int32_t row_lo = (int32_t)max(i_full0, (int64_t)INT32_MIN), row_hi = (int32_t)min(i_full1, (int64_t)INT32_MAX);
 
   // ---- main rows
   int q = 0;
@@ -400,7 +405,8 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
       const uint4 xo = mask_tail(funnel16<DL>(*reinterpret_cast<const uint4*>(st + kRowsBytes + rr * kSpan),
                                               *reinterpret_cast<const uint4*>(st + kRowsBytes + rr * kSpan + 16)));
       const uint4 xc = xc_next;
-      if (q + 1 < nrows) cptr += p.in_pitch;  // the last row re-reads itself (harmless)
+      asm volatile("" : "+l"(in_pitch), "+l"(out_pitch), "+r"(store_mode), "+r"(row_lo), "+r"(row_hi));
+      if (q + 1 < nrows) cptr += in_pitch;  // the last row re-reads itself (harmless)
       xc_next = load_centre(cptr, true);
       // vertical update
 #pragma unroll
@@ -468,7 +474,7 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
       // of the certified decision
       uint32_t nrow = (uint32_t)p.h;
       float inv_nrow = p.inv_h;
-      if (i < i_full0 || i > i_full1) {
+      if ((int32_t)i < row_lo || (int32_t)i > row_hi) {
         nrow = (uint32_t)(min(i + p.u, p.H_global - 1) - max(i - p.o, (int64_t)-1));
         inv_nrow = __frcp_rn((float)nrow);
       }
@@ -569,9 +575,9 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
         }
       }
       // ---- store the mask: outputs j0 .. j0+15 (j0 is a multiple of 16)
-      if (valid_lane) {
-        if (p.fmt == 0) {
-          if (out_vec) {
+      if (store_mode != 0u) {
+        if (store_mode != 3u) {
+          if (store_mode == 1u) {
             __stcs(reinterpret_cast<uint4*>(optr), make_uint4(wv[0], wv[1], wv[2], wv[3]));  // streaming
           } else {
 #pragma unroll
@@ -588,7 +594,7 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
           if (vmask >> 8) optr[1] = (uint8_t)(mb & 0xFFu);
         }
       }
-      optr += p.out_pitch;
+      optr += out_pitch;
     }
     stage_end(s);
   }
