@@ -102,6 +102,14 @@ __device__ __forceinline__ uint64_t scan_step(uint64_t v, int off) {
   return ((uint64_t)hi << 32) | lo;
 }
 
+// A warp-uniform value the compiler must keep in a register (a shuffle result
+// cannot be re-materialised from the kernel-parameter bank).
+__device__ __forceinline__ int64_t opaque(int64_t v) {
+  const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, 0);
+  const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)((uint64_t)v >> 32), 0);
+  return (int64_t)(((uint64_t)hi << 32) | lo);
+}
+
 // value of lane `src` (0 if src < 0: columns left of the strip are zero)
 __device__ __forceinline__ uint32_t shfl_idx(uint32_t v, int src) {
   const uint32_t r = __shfl_sync(0xffffffffu, v, src & 31);
@@ -385,9 +393,14 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
   constexpr int method = METHOD;
   // rows whose window is clipped by the top / bottom image edge: nrow < h
   const int64_t i_full0 = p.o - 1, i_full1 = p.H_global - 1 - p.u;  // nrow == h for i in [i_full0, i_full1]
-  // per-row scalars kept in registers (the compiler would otherwise re-load
-  // them from the parameter bank every row, exposing the load latency)
-  int64_t in_pitch = p.in_pitch, out_pitch = p.out_pitch;
+  // per-row scalars kept in registers: passed through a shuffle, ptxas cannot
+  // re-materialise them from the parameter bank every row (which exposed the
+  // load latency in the row loop)
+  // (not for the uint64 variant: its register budget is tighter and the
+  // extra live registers cost more than the re-loads)
+  const int64_t in_pitch = D64 ? p.in_pitch : opaque(p.in_pitch);
+  const int64_t out_pitch = D64 ? p.out_pitch : opaque(p.out_pitch);
+  const float inv_h = D64 ? p.inv_h : __int_as_float((int)opaque((int64_t)__float_as_int(p.inv_h)));
   uint32_t store_mode = !valid_lane ? 0u : (p.fmt != 0 ? 3u : (out_vec ? 1u : 2u));
   int32_t row_lo = (int32_t)max(i_full0, (int64_t)INT32_MIN), row_hi = (int32_t)min(i_full1, (int64_t)INT32_MAX);
 
@@ -405,7 +418,6 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
       const uint4 xo = mask_tail(funnel16<DL>(*reinterpret_cast<const uint4*>(st + kRowsBytes + rr * kSpan),
                                               *reinterpret_cast<const uint4*>(st + kRowsBytes + rr * kSpan + 16)));
       const uint4 xc = xc_next;
-      asm volatile("" : "+l"(in_pitch), "+l"(out_pitch), "+r"(store_mode), "+r"(row_lo), "+r"(row_hi));
       if (q + 1 < nrows) cptr += in_pitch;  // the last row re-reads itself (harmless)
       xc_next = load_centre(cptr, true);
       // vertical update
@@ -473,7 +485,7 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
       // c_t = c_{t-1} + C[a+t] - C[a+t-w] fused with stage 1
       // of the certified decision
       uint32_t nrow = (uint32_t)p.h;
-      float inv_nrow = p.inv_h;
+      float inv_nrow = inv_h;
       if ((int32_t)i < row_lo || (int32_t)i > row_hi) {
         nrow = (uint32_t)(min(i + p.u, p.H_global - 1) - max(i - p.o, (int64_t)-1));
         inv_nrow = __frcp_rn((float)nrow);
