@@ -357,15 +357,19 @@ def ours_main(args):
                 hout.copy_(out, non_blocking=True)
             h2d, d2h = host_own.numel(), hout.numel()
         else:
-            hin = torch.from_numpy(pages_np).pin_memory()
-            hout = torch.empty((P, H, cols), dtype=torch.uint8).pin_memory()
+            # a bounded slice of the batch keeps the pinned host memory per rank
+            # small (eight ranks of 64 pages would pin ~36 GB); the metric is a
+            # rate, the per-page cost is the same
+            Pe = min(P, 16)
+            hin = torch.from_numpy(np.ascontiguousarray(pages_np[:Pe])).pin_memory()
+            hout = torch.empty((Pe, H, cols), dtype=torch.uint8).pin_memory()
 
             def e2e_step():
                 # abin_binarize_batched with ABIN_HOST_IO: the library streams
                 # the pages through device staging, copies overlapped with compute
                 rc = abin.raw().abin_binarize_batched(
                     abin.METHODS[method], abin.ctypes.c_void_p(hin.data_ptr()), hin.stride(0),
-                    abin.ctypes.c_void_p(hout.data_ptr()), hout.stride(0), P, H, W, hin.stride(1), hout.stride(1),
+                    abin.ctypes.c_void_p(hout.data_ptr()), hout.stride(0), Pe, H, W, hin.stride(1), hout.stride(1),
                     abin.MASK_BITS if packed else abin.MASK_U8, h, w, k, R, -1, flags | abin.HOST_IO, None,
                     abin.ctypes.c_void_p(cs.cuda_stream))
                 if rc != 0:
@@ -387,9 +391,11 @@ def ours_main(args):
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e_ms = float(et.item()) / e2e_steps
-        ok = torch.equal(hout, out.cpu())
-        e2e = {"value": px_total / (e2e_ms / 1e3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+        e2e_px = (hout.shape[0] * H * W if not banded else px_rank) * world
+        ok = torch.equal(hout, out.cpu() if banded else out[:hout.shape[0]].cpu())
+        e2e = {"value": e2e_px / (e2e_ms / 1e3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms, "steps": e2e_steps,
+               "pages_per_rank": None if banded else int(hout.shape[0]),
                "matches_device_path": bool(ok)}
 
     if rank == 0:

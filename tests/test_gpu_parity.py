@@ -386,3 +386,12 @@ def test_otsu_equals_oracle():
             assert np.array_equal(m.cpu().numpy(), ref)
         mb, _ = ab.otsu(to_dev(I), packed=True)
         assert np.array_equal(mb.cpu().numpy(), oracle.pack_bits(ref))
+
+
+def test_wide_window_kernel():
+    """Effective windows wider than 495 columns take the CTA-strip kernel
+    (moments_wide.cuh): Sauvola / Niblack / Wolf against the oracle."""
+    I = synth.page(150, 1400, synth.config_seed(7, 77), stain=True)
+    for method in ("sauvola", "niblack", "wolf"):
+        check_full(method, I, 33, 601, stats=False)
+        check_full(method, I, 8, 1000, packed=True, stats=False)
