@@ -270,7 +270,9 @@ def ours_main(args):
         def step(i):
             adist.run_band(method, band, h, w, k, R, packed=packed, out=out, flags=flags, counters=counters,
                            rank=rank, world=world)
-        launches_per_step = 3
+        # per binarize_band call: the v4 moments kernel, the exact fixup and the
+        # (normally empty) v3 overflow follow-up; three calls per band
+        launches_per_step = 3 * 3
         l2_note = f"band of {rows} rows per rank ({px_rank / 1e9:.2f} GB) > L2: no flush needed"
         pages_np = None
     else:
@@ -296,7 +298,10 @@ def ours_main(args):
                     ab.sauvola(x[0], h, w, k, R, packed=packed, out=o[0], flags=flags, counters=counters)
             else:
                 ab.binarize_batched(method, x, h, w, k, R, packed=packed, out=o, flags=flags, counters=counters)
-        launches_per_step = 1
+        # quantile: one kernel; moments: v4 + exact fixup + v3 overflow
+        # follow-up (its CTAs exit at once unless the fixup queue overflowed);
+        # Wolf adds the fill + global-minimum pre-pass
+        launches_per_step = 1 if method == "quantile" else (5 if method == "wolf" else 3)
         l2_note = (f"inputs {step_bytes / 1e9:.2f} GB per rank per step > L2: no flush needed" if n_copies == 1 else
                    f"L2-resident workload: steps rotate through {n_copies} input/mask copies "
                    f"({n_copies * step_bytes / 1e6:.0f} MB > 126 MB L2), no step reuses a cached page")

@@ -14,6 +14,7 @@
 #include "../../include/abin.h"
 #include "globalmin.cuh"
 #include "otsu.cuh"
+#include "fixup.cuh"
 #include "launch.cuh"
 #include "quantile.cuh"
 
@@ -295,7 +296,31 @@ int encode_map_chunks(const MomCall& c, int chunks, int rows, CUtensorMap* map) 
   return ABIN_OK;
 }
 
+// The library's scratch (fixup queue, Wolf minima, rule accumulators) comes
+// from the device's default stream-ordered pool.  Keep up to 512 MB of it
+// cached across calls (the default threshold 0 hands it back to the driver
+// at every synchronisation, and the next call pays for re-mapping it).
+static void keep_pool_warm() {
+  static std::mutex mu;
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::lock_guard<std::mutex> g(mu);
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (thr < (512ull << 20)) {
+      thr = 512ull << 20;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  done[dev] = true;
+}
+
 int run_moments(const MomCall& c) {
+  keep_pool_warm();
   const Window win = effective_window(c.h, c.w, c.H_global, c.W);
   if ((uint64_t)win.h > 66051u) return ABIN_ERANGE;  // column D_j must fit uint32 (255^2 h < 2^32)
   const int KH = (win.w + 1 + kG - 1) / kG;
@@ -306,11 +331,22 @@ int run_moments(const MomCall& c) {
   // generic loader stages the rows.
   const bool tma_ok = !((reinterpret_cast<uintptr_t>(c.in) & 15u) || (c.in_pitch & 15) ||
                         (c.n_pages > 1 && (c.in_page_stride & 15))) && !(c.flags & ABIN_NO_TMA_INTERNAL);
+  // window sums c are uint32 in the kernels: exact while 255 h w < 2^32
+  if ((uint64_t)255 * (uint64_t)win.h * (uint64_t)win.w >= (1ull << 32)) return ABIN_ERANGE;
   const bool rule = c.method >= ABIN_FENG && c.method <= ABIN_PHANSALKAR;
-  const bool use_v4 = fast && tma_ok && !(c.flags & ABIN_V3_INTERNAL) && !rule;
-  CUtensorMap map;
-  int rc = use_v4 ? encode_map_chunks(c, v4::kChunks, v4::kR, &map)
-                  : encode_map(c, fast ? kR : (nt_wide == 128 ? 8 : 4), tma_ok, &map);
+  const bool stats = c.c_out || c.d_out || c.n_out || c.t_out || c.mask_out;
+  // v4 (warp CTAs, certified fp32 + deferred exact fixup) for the production
+  // path; the v3 kernel (inline exact path) for rules, statistics, forced fp64,
+  // rows TMA cannot stage, and bit masks whose 32-bit words are not aligned
+  // (the fixup patches bits with 32-bit atomics)
+  const bool words_ok = c.fmt == ABIN_MASK_U8 ||
+      ((reinterpret_cast<uintptr_t>(c.out) | (uintptr_t)c.out_pitch |
+        (uintptr_t)(c.n_pages > 1 ? c.out_page_stride : 0)) & 3u) == 0;
+  const bool use_v4 = fast && tma_ok && !(c.flags & ABIN_V3_INTERNAL) && !rule && !stats &&
+                      !(c.flags & ABIN_FORCE_FP64) && words_ok;
+  CUtensorMap map, map4;
+  int rc = encode_map(c, fast ? kR : (nt_wide == 128 ? 8 : 4), tma_ok, &map);
+  if (rc == ABIN_OK && use_v4) rc = encode_map_chunks(c, v4::kChunks, v4::kR, &map4);
   if (rc) return rc;
 
   unsigned int* Lw = nullptr;
@@ -345,7 +381,7 @@ int run_moments(const MomCall& c) {
   }
   const bool d64 = (c.flags & ABIN_FORCE_U64_SQ) || (uint64_t)win.h * (uint64_t)win.w * 65025u >= (1ull << 32);
   const int ph = ((-win.w) % 4 + 4) % 4;
-  const bool stats = c.c_out || c.d_out || c.n_out || c.t_out || c.mask_out;
+  uint4* queue = nullptr;
 
   if (fast) {
     MomParams p;
@@ -374,28 +410,57 @@ int run_moments(const MomCall& c) {
     p.c_out = c.c_out; p.d_out = c.d_out; p.n_out = c.n_out; p.t_out = c.t_out; p.mask_out = c.mask_out;
     p.stats = stats ? 1 : 0;
     const int w32 = win.w % 32;
+    const int64_t n_tiles3 = (int64_t)p.n_strips * p.n_bands * c.n_pages;
     if (use_v4) {
+      MomParams q = p;
       // one warp per CTA; a strip = one warp's 32 - KH valid lanes
-      p.n_strips = (int32_t)((c.W + p.Tw - 1) / p.Tw);
+      q.n_strips = (int32_t)((c.W + q.Tw - 1) / q.Tw);
       // strips whose windows stay inside [0, W) (ncol = w) are
       // [sL, sR); the others take the border variant of the kernel
-      const int64_t Tw = p.Tw;
-      const int64_t sL = std::min<int64_t>(p.n_strips, win.l - 1 > 0 ? (win.l - 1 + Tw - 1) / Tw : 0);
+      const int64_t Tw = q.Tw;
+      const int64_t sL = std::min<int64_t>(q.n_strips, win.l - 1 > 0 ? (win.l - 1 + Tw - 1) / Tw : 0);
       const int64_t nfit = (c.W - win.r - Tw) >= 0 ? (c.W - win.r - Tw) / Tw + 1 : 0;
-      p.sL = (int32_t)sL;
-      p.sR = (int32_t)std::max<int64_t>(sL, std::min<int64_t>(nfit, p.n_strips));
-      p.n_pages_v4 = (int32_t)c.n_pages;
-      choose_bands_v4((int64_t)p.n_strips * c.n_pages, c.H_out, win.h, 148 * 16, &p.B, &p.n_bands);
+      q.sL = (int32_t)sL;
+      q.sR = (int32_t)std::max<int64_t>(sL, std::min<int64_t>(nfit, q.n_strips));
+      q.n_pages_v4 = (int32_t)c.n_pages;
+      choose_bands_v4((int64_t)q.n_strips * c.n_pages, c.H_out, win.h, 148 * 16, &q.B, &q.n_bands);
       if (const char* nb = getenv("ABIN_V4_BANDS")) {  // experiments: force the band count
         const int64_t want = std::max<int64_t>(1, std::min<int64_t>(atoll(nb), c.H_out));
-        p.B = (int32_t)((c.H_out + want - 1) / want);
-        p.n_bands = (int32_t)((c.H_out + p.B - 1) / p.B);
+        q.B = (int32_t)((c.H_out + want - 1) / want);
+        q.n_bands = (int32_t)((c.H_out + q.B - 1) / q.B);
       }
-      const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * c.n_pages;
-      rc = launch_v4_any(w32, d64, map, p, n_tiles, c.stream);
+      // the exact-fixup queue: 16 bytes per ambiguous lane (16 pixels)
+      uint32_t cap = 1u << 20;
+      if (const char* qc = getenv("ABIN_QUEUE_CAP"))  // tests: exercise the overflow follow-up
+        cap = (uint32_t)std::max<long long>(1, std::min<long long>(atoll(qc), 1ll << 26));
+      CK(cudaMallocAsync(&queue, (size_t)cap * 16 + 16, c.stream));
+      uint32_t* qcount = reinterpret_cast<uint32_t*>(queue + (size_t)cap);
+      CK(cudaMemsetAsync(qcount, 0, 4, c.stream));
+      q.q_data = queue;
+      q.q_count = qcount;
+      q.q_cap = cap;
+      const int64_t n_tiles = (int64_t)q.n_strips * q.n_bands * c.n_pages;
+      rc = launch_v4_any(w32, d64, map4, q, n_tiles, c.stream);
+      if (rc == ABIN_OK) {
+        const size_t fsm = fixup_smem_bytes(win.w);
+        if (fsm > 48 * 1024) CK(cudaFuncSetAttribute(k_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fixup, kFixNT, fsm));
+        k_fixup<<<148 * std::max(1, per_sm), kFixNT, fsm, c.stream>>>(q);
+        CK(cudaGetLastError());
+        // overflow (pathological inputs only): the v3 kernel redoes the call
+        // exactly; its CTAs return at once when the queue held everything
+        p.ovf_count = qcount;
+        p.ovf_cap = cap;
+        // about one CTA per SM: the (normal) empty launch costs little
+        const int64_t per_band = (int64_t)p.n_strips * c.n_pages;
+        const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(c.H_out, 148 / per_band));
+        p.B = (int32_t)((c.H_out + nb - 1) / nb);
+        p.n_bands = (int32_t)((c.H_out + p.B - 1) / p.B);
+        rc = launch_fast_any(w32, d64, map, p, per_band * p.n_bands, c.stream);
+      }
     } else {
-      const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * c.n_pages;
-      rc = launch_fast_any(w32, d64, map, p, n_tiles, c.stream);
+      rc = launch_fast_any(w32, d64, map, p, n_tiles3, c.stream);
     }
   } else {
     wide::MomParams p;
@@ -428,6 +493,10 @@ int run_moments(const MomCall& c) {
   }
   if (acc) {
     cudaError_t e = cudaFreeAsync(acc, c.stream);
+    if (rc == ABIN_OK && e != cudaSuccess) return cuda_fail(e);
+  }
+  if (queue) {
+    cudaError_t e = cudaFreeAsync(queue, c.stream);
     if (rc == ABIN_OK && e != cudaSuccess) return cuda_fail(e);
   }
   return rc;

@@ -68,6 +68,13 @@ struct MomParams {
   int32_t counters_n;        // 2, or 3 with ABIN_COUNT_STAGES
   int32_t sL, sR;            // v4: strips [sL, sR) are interior (no image border inside their windows)
   RuleParams rp;             // Table 1 rules Feng / Rais / Khurshid / Phansalkar (rules.cuh)
+  // v4 -> exact fixup queue (fixup.cuh): one uint4 per ambiguous lane, q_count appends
+  uint4* q_data;
+  uint32_t* q_count;
+  uint32_t q_cap;
+  // v3 as the overflow follow-up: run only if *ovf_count > ovf_cap
+  const uint32_t* ovf_count;
+  uint32_t ovf_cap;
   int32_t n_pages_v4;        // v4: pages of the launch
   // statistics mode (page 0 only)
   uint64_t* c_out;
@@ -293,6 +300,7 @@ __global__ void __launch_bounds__(kNT, 4) k_moments(const __grid_constant__ CUte
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(nic_all + kCW * kWarpRow);
   uint32_t* done_cnt = reinterpret_cast<uint32_t*>(full_bar + kNS);  // warps finished with a slot
 
+  if (p.ovf_count != nullptr && *p.ovf_count <= p.ovf_cap) return;  // follow-up launch, no queue overflow
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
 

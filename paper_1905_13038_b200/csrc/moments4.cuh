@@ -160,85 +160,6 @@ __device__ __forceinline__ float refined_bound(const MomParams& p, float s) {
   return __fmaf_rn(p.rb1, fminf(p.rsdv, p.rdv * rs), p.rb0) * 1.000001f;
 }
 
-// Rare path (stages 2 and 3) for one lane-row: re-derives c_t, d_t from the
-// anchor and the published column sums (shared memory), re-tests stage 1,
-// and decides the still ambiguous pixels exactly.  Returns the decided bits
-// in fix / fixv.  Everything it needs beyond a few scalars comes from shared
-// memory, so it costs the hot loop no registers (a call would: the ABI spills
-// the live column sums around a call site).
-template <int METHOD, int PH, typename DT>
-__device__ __forceinline__ void rare_path(const MomParams& p, const uint32_t* cb, const uint32_t* db, int lane,
-                                       int st0, uint32_t Ac, DT Ad, uint4 xc, uint32_t amb,
-                                       int64_t i, int64_t j0, uint32_t nrow, float inv_nrow, bool edge,
-                                       const float* nicw, float nic_c, float Lf, int page, uint32_t* fix_out,
-                                       uint32_t* fixv_out, uint64_t* cnt) {
-  const bool slow_all = p.stats || p.force_fp64;
-  constexpr int method = METHOD;
-  uint32_t fix = 0, fixv = 0;
-  uint32_t cc = Ac;
-  DT dd = Ad;
-#pragma unroll 1
-  for (int t = 0; t < kG; ++t) {
-    const int lc = st0 + PH + t;  // leaving column (strip-relative)
-    const uint32_t Cl = lc < 0 ? 0u : cb[swz(lc)], Dl = lc < 0 ? 0u : db[swz(lc)];
-    const int own = swz(kG * lane + t);
-    cc += cb[own] - Cl;
-    dd += (DT)db[own] - (DT)Dl;
-    if (!((amb >> t) & 1u)) continue;
-    const float nu = (edge ? nicw[own] : nic_c) * inv_nrow;
-    const uint32_t wd = (t >> 2) == 0 ? xc.x : ((t >> 2) == 1 ? xc.y : ((t >> 2) == 2 ? xc.z : xc.w));
-    const uint32_t I = (wd >> (8 * (t & 3))) & 0xFFu;
-    if (!slow_all) {
-      float sv;
-      const float e = stage1_e(method, to_f(cc), to_f(dd), nu, (float)I, p.fa, p.fb, Lf, sv);
-      if (!(fabsf(e) < p.delta1)) continue;  // stage 1 decided this one
-      // the same bound with the data-dependent |s~ - s|:
-      // the stage-1 sign stands if |e| clears it
-      if (fabsf(e) * 0.999999f >= refined_bound(p, sv)) continue;
-    }
-    const int64_t j = j0 + t;
-    const uint32_t ncol = (uint32_t)max((int64_t)1, min(j + p.r, p.W - 1) - max(j - p.l, (int64_t)-1));
-    const uint32_t n = ncol * nrow;
-    const uint64_t c64 = (uint64_t)cc;
-    const uint64_t d64 = (uint64_t)dd;
-    bool decided = false;
-    uint32_t mk = 0;
-    if (!slow_all) {
-      cnt[2]++;
-      // stage 2: exact V = n d - c^2 >= 0, fp32 with the tight bound delta2
-      const uint64_t V = (uint64_t)n * d64 - c64 * c64;
-      const float Vf = __fmaf_rn((float)(uint32_t)(V >> 32), 4294967296.0f, (float)(uint32_t)V);
-      const float invn = __frcp_rn((float)n);
-      const float m = (float)(uint32_t)c64 * invn;
-      const float t2 = threshold_f32(method, m, sqrt_approx(Vf) * invn, p.fa, p.fb, Lf);
-      const float e2 = t2 - (float)I;
-      if (fabsf(e2) >= p.delta2) {
-        decided = true;
-        mk = e2 < 0.0f ? 1u : 0u;
-      }
-    }
-    double tt = 0.0;
-    if (!decided) {
-      tt = threshold_fp64(method, c64, d64, n, p.k, p.R, (double)Lf);
-      mk = ((double)I <= tt) ? 0u : 1u;
-      cnt[1]++;
-      if (fabs((double)I - tt) < 1e-9) cnt[0]++;
-    }
-    fix |= 1u << t;
-    fixv |= mk << t;
-    if (p.stats && page == 0) {
-      const int64_t idx = (i - p.row0) * p.W + j;
-      if (p.c_out) p.c_out[idx] = c64;
-      if (p.d_out) p.d_out[idx] = d64;
-      if (p.n_out) p.n_out[idx] = n;
-      if (p.t_out) p.t_out[idx] = tt;
-      if (p.mask_out) p.mask_out[idx] = (uint8_t)mk;
-    }
-  }
-  *fix_out = fix;
-  *fixv_out = fixv;
-}
-
 // Kernel template parameters:
 //   W32   w mod 32: fixes the phase PH = (-w) mod 4 of the leaving reads and
 //         the byte funnel DL = r mod 16 of the staged rows
@@ -304,7 +225,6 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
     lofs[g] = (s < 0 || s >= kStrip) ? kZero : swz(s);
   }
   const float Lf = (METHOD == M_WOLF) ? (float)(p.L_fixed >= 0 ? p.L_fixed : (int)p.L_page[page]) : 0.0f;
-  const bool slow_all = p.stats || p.force_fp64;
   const float nic_c = -__frcp_rn((float)p.w);             // interior: ncol = w
   uint32_t km[4] = {~0u, ~0u, ~0u, ~0u};                  // bytes of columns >= W (edge strips)
   if (EDGE) {
@@ -349,7 +269,6 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
   uint32_t C[kG], D[kG];
 #pragma unroll
   for (int t = 0; t < kG; ++t) C[t] = D[t] = 0;
-  uint64_t cnt[3] = {0, 0, 0};  // near ties, fp64 fallbacks, stage-2 pixels
 
   // ---- warm-up: rows y0-o .. y0+u-1
   for (int s = 0; s < WS; ++s) {
@@ -566,25 +485,17 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
       }
       // ambiguous lane: some pixel within the certified bound, evaluated with the
       // lane's smallest s~ (the data-dependent bound decreases in s~)
-      uint32_t amb = slow_all ? vmask : 0u;
+      uint32_t amb = 0u;
       if (emin < p.delta1) {  // coarse test first (rare for Sauvola)
-        const float dlane = refined_bound(p, smin);
-        if (emin * 0.999999f < dlane) amb = vmask;
+        if (emin * 0.999999f < refined_bound(p, smin)) amb = vmask;
       }
-      if (__any_sync(0xffffffffu, amb != 0u)) {
-        uint32_t fix = 0, fixv = 0;
-        if (amb)
-          rare_path<METHOD, PH, DT>(p, cb, db, lane, st0, Ac, Ad, xc, amb, i, j0, nrow, inv_nrow, EDGE, nicw, nic_c, Lf, page,
-                            &fix, &fixv, cnt);
-        if (fix) {
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            // spread 4 bits into the 4 bytes of a word: bit b -> byte b
-            const uint32_t fm = (((fix >> (4 * g)) & 0xFu) * 0x00204081u) & 0x01010101u;
-            const uint32_t fv = (((fixv >> (4 * g)) & 0xFu) * 0x00204081u) & 0x01010101u;
-            wv[g] = (wv[g] & ~(fm * 0xFFu)) | fv;
-          }
-        }
+      // ambiguous lanes (rare) go to the exact fixup kernel (fixup.cuh), which
+      // recomputes their pixels' sums and decides them exactly, overwriting
+      // the provisional bits stored below; nothing of the exact stages lives
+      // in this kernel: its registers go to the hot loop
+      if (amb) {
+        const uint32_t slot = atomicAdd(p.q_count, 1u);
+        if (slot < p.q_cap) p.q_data[slot] = make_uint4((uint32_t)page, (uint32_t)(i - p.row0), (uint32_t)j0, amb);
       }
       // ---- store the mask: outputs j0 .. j0+15 (j0 is a multiple of 16)
       if (store_mode != 0u) {
@@ -611,15 +522,6 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
     stage_end(s);
   }
 
-  if (p.counters) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-      for (int z = 0; z < 3; ++z) cnt[z] += __shfl_down_sync(0xffffffffu, cnt[z], off);
-    if (lane == 0)
-      for (int z = 0; z < p.counters_n && z < 3; ++z)
-        if (cnt[z]) atomicAdd(reinterpret_cast<unsigned long long*>(&p.counters[z]), (unsigned long long)cnt[z]);
-  }
 }
 
 // One launch for all strips: the border strips (slower: per-column counts)

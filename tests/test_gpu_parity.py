@@ -395,3 +395,34 @@ def test_wide_window_kernel():
     for method in ("sauvola", "niblack", "wolf"):
         check_full(method, I, 33, 601, stats=False)
         check_full(method, I, 8, 1000, packed=True, stats=False)
+
+
+@pytest.mark.parametrize("packed", [False, True])
+@pytest.mark.parametrize("cap", [None, 1, 5000])
+def test_fixup_queue_and_overflow(monkeypatch, packed, cap):
+    """The v4 kernel queues the pixels its fp32 filter cannot decide; the
+    fixup kernel decides them exactly.  On a near-constant page Niblack's
+    threshold equals most pixel values (near ties everywhere), so the queue
+    holds tens of thousands of pixels: cap=None is the production queue,
+    cap=1 / 5000 force the overflow follow-up (the v3 kernel re-does the call
+    exactly).  All three: masks bit-exact vs the oracle, near ties counted
+    exactly once."""
+    if cap is not None:
+        monkeypatch.setenv("ABIN_QUEUE_CAP", str(cap))
+    rng = np.random.default_rng(17)
+    P, H, W = 3, 300, 704
+    pages = np.full((P, H, W), 128, np.uint8)
+    sel = rng.random((P, H, W)) < 2e-4
+    pages[sel] = rng.integers(0, 256, int(sel.sum()), dtype=np.uint8)
+    buf = torch.zeros((P, H, W), dtype=torch.uint8, device=DEV)
+    buf.copy_(torch.from_numpy(pages))
+    cnt = torch.zeros(2, dtype=torch.int64, device=DEV)
+    m = ab.binarize_batched("niblack", buf, 31, 31, -0.2, 128.0, packed=packed, counters=cnt).cpu().numpy()
+    near = 0
+    for p in range(P):
+        ref = oracle.binarize("niblack", pages[p], 31, 31, -0.2, 128.0, stats=True)
+        want = oracle.pack_bits(ref["mask"]) if packed else ref["mask"]
+        assert np.array_equal(m[p], want), (p, int((m[p] != want).sum()))
+        near += ref["near_tie"]
+    assert near > 10_000
+    assert int(cnt[0]) == near
