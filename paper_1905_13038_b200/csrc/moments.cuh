@@ -61,7 +61,7 @@ struct MomParams {
   // fp32 filter constants (host-derived, K2)
   float fa, fb;              // Sauvola: 1-k, k/R;  Niblack: -, k;  Wolf: k, 1/R
   float delta1, delta2;      // certified bounds of the two fp32 stages (incl. the fp64 error)
-  float rb0, rb1, rdv, rsdv; // v4 rare path: data-dependent stage-1 bound rb0 + rb1 min(rsdv, rdv / s~)
+  float rb0, rb1, rdv, rsdv; // v4 ambiguity test: data-dependent stage-1 bound rb0 + rb1 min(rsdv, rdv / s~)
   float inv_h;               // fl(1/h): 1/nrow for interior rows
   int32_t stats;             // statistics mode: every pixel takes the fp64 sequence
   uint64_t* counters;        // [near_tie, fp64 fallbacks(, stage-2 pixels)] or null

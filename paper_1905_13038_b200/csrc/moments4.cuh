@@ -40,11 +40,12 @@
 //  * Epilogue (Alg. 1 l.118-124, Table 1; DESIGN.md section 5 "certified
 //    decision"), fused with the recursion pixel pair by pixel pair: stage 1
 //    evaluates t~ in fp32 (FFMA2 pairs) from the exact c, d; lanes with a
-//    pixel |I - t~| < delta1 call the rare path, which re-derives c, d from
-//    the published row: stage 2 in fp32 from the exact V = n d - c^2 (bound
-//    delta2), stage 3 the canonical IEEE double sequence.  The mask equals the
-//    double-precision decision bit for bit; near ties |I - t| < 1e-9 are
-//    counted on stage 3.
+//    pixel within the certified bound store provisional bits and are queued
+//    for k_fixup (fixup.cuh), which recomputes their c, d from the image and
+//    decides them exactly: stage 2 in fp32 from the exact V = n d - c^2
+//    (bound delta2), stage 3 the canonical IEEE double sequence.  The mask
+//    equals the double-precision decision bit for bit; near ties
+//    |I - t| < 1e-9 are counted on stage 3.
 #pragma once
 #include <cstdint>
 #include <cuda.h>
