@@ -111,6 +111,14 @@ __device__ __forceinline__ int64_t opaque(int64_t v) {
   return (int64_t)(((uint64_t)hi << 32) | lo);
 }
 
+// value of lane `src & 31` (no range select)
+__device__ __forceinline__ uint32_t shfl_raw(uint32_t v, int src) { return __shfl_sync(0xffffffffu, v, src & 31); }
+__device__ __forceinline__ uint64_t shfl_raw(uint64_t v, int src) {
+  const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src & 31);
+  const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src & 31);
+  return ((uint64_t)hi << 32) | lo;
+}
+
 // value of lane `src` (0 if src < 0: columns left of the strip are zero)
 __device__ __forceinline__ uint32_t shfl_idx(uint32_t v, int src) {
   const uint32_t r = __shfl_sync(0xffffffffu, v, src & 31);
@@ -375,13 +383,17 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
         if (mW <= 8) {
           // small windows: sum the m lanes' totals directly -- m + 1 independent
           // shuffles instead of a dependent 5-level scan
-          uint32_t ac = 0u - shfl_idx(sc, lane - mW);
-          DT ad = (DT)0 - shfl_idx(sd, lane - mW);
+          // (only the output lanes' start values matter, and for them every
+          // source lane k - q >= k - m >= KH - m >= 0: no zero-select needed;
+          // the halo lanes read wrapped-around garbage they never use)
+          uint32_t ac = 0u - shfl_raw(sc, lane - mW);
+          DT ad = (DT)0 - shfl_raw(sd, lane - mW);
 #pragma unroll
           for (int q = 1; q <= 8; ++q) {
-            if (q > mW) break;
-            ac += shfl_idx(tc, lane - q);
-            ad += shfl_idx(td, lane - q);
+            if (q <= mW) {  // warp-uniform: predicated, independent shuffles
+              ac += shfl_raw(tc, lane - q);
+              ad += shfl_raw(td, lane - q);
+            }
           }
           Ac = ac;
           Ad = ad;
