@@ -195,7 +195,7 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
   const int64_t XC = J0 - (int64_t)kG * p.KH;             // = Sw - r, centre-row chunk origin (aligned)
   const int64_t y0 = p.row0 + (int64_t)band * p.B;        // first output row (global)
   const int nrows = (int)min((int64_t)p.B, p.row0 + p.H_out - y0);
-  const int WS = (p.h + kR - 1) / kR;                     // warm-up stages
+  const int WS = (p.h + 2 * kR - 1) / (2 * kR);           // warm-up stages (2 kR rows: both streams' buffers)
   const int total = WS + (nrows + kR - 1) / kR;
 
   // ---- TMA: one box per stream and stage, chunks [XE/16, XE/16 + 33) x kR rows
@@ -204,10 +204,11 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
     const int slot = s % kNS;
     uint8_t* st = ring + slot * kStageBytes;
     const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
-    if (s < WS) {
-      mbar_arrive_expect_tx(&full[slot], kR * kSpan);
-      tma_load_4d_hint(st, &tin, 0, xchunk, (int32_t)(y0 - p.o + (int64_t)s * kR - p.buf_row0), page, &full[slot],
-                       keep);
+    if (s < WS) {  // warm-up rows y0-o+2kR s .. +2kR-1 into both halves of the slot
+      const int32_t yw = (int32_t)(y0 - p.o + (int64_t)s * 2 * kR - p.buf_row0);
+      mbar_arrive_expect_tx(&full[slot], 2 * kR * kSpan);
+      tma_load_4d_hint(st, &tin, 0, xchunk, yw, page, &full[slot], keep);
+      tma_load_4d_hint(st + kRowsBytes, &tin, 0, xchunk, yw + kR, page, &full[slot], keep);
     } else {
       const int64_t q0 = (int64_t)(s - WS) * kR;
       mbar_arrive_expect_tx(&full[slot], 2 * kR * kSpan);
@@ -283,11 +284,12 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
   for (int s = 0; s < WS; ++s) {
     mbar_wait(&full[s % kNS], (s / kNS) & 1);
     const uint8_t* st = ring + (s % kNS) * kStageBytes + eo;
-    const int nr = min(kR, p.h - s * kR);
+    const int nr = min(2 * kR, p.h - s * 2 * kR);
 #pragma unroll 1
     for (int rr = 0; rr < nr; ++rr) {
-      const uint4 x = mask_tail(funnel16<DL>(*reinterpret_cast<const uint4*>(st + rr * kSpan),
-                                             *reinterpret_cast<const uint4*>(st + rr * kSpan + 16)));
+      const uint8_t* sr = st + (rr < kR ? rr * kSpan : kRowsBytes + (rr - kR) * kSpan);
+      const uint4 x = mask_tail(funnel16<DL>(*reinterpret_cast<const uint4*>(sr),
+                                             *reinterpret_cast<const uint4*>(sr + 16)));
 #pragma unroll
       for (int t = 0; t < kG; ++t) {
         const uint32_t v = byte_of(x, t);
@@ -486,7 +488,7 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
               e = __ffma2_rn(ka, b, __fadd2_rn(I, mn));                                              // I - t
             }
             emin = fminf(emin, fminf(fabsf(e.x), fabsf(e.y)));
-            smin = fminf(smin, fminf(sv.x, sv.y));
+            if (METHOD == M_NIBLACK) smin = fminf(smin, fminf(sv.x, sv.y));
             e4[h2] = e.x;
             e4[h2 + 1] = e.y;
           }
@@ -496,11 +498,15 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
           wv[g] = ~__byte_perm(lo, hi, 0x7610u) & 0x01010101u;
         }
       }
-      // ambiguous lane: some pixel within the certified bound, evaluated with the
-      // lane's smallest s~ (the data-dependent bound decreases in s~)
+      // ambiguous lane: some pixel within the certified bound delta1.  For
+      // Niblack (t = m + k s: the bound's sqrt(dv) term is large next to the
+      // residuals) the lane is re-tested with the data-dependent bound at its
+      // smallest s~ (the bound decreases in s~), which keeps the queue ~40x
+      // shorter; for Sauvola / Wolf the coarse test alone queues next to
+      // nothing, and tracking s~ would cost more than it saves
       uint32_t amb = 0u;
-      if (emin < p.delta1) {  // coarse test first (rare for Sauvola)
-        if (emin * 0.999999f < refined_bound(p, smin)) amb = vmask;
+      if (emin < p.delta1) {
+        if (METHOD != M_NIBLACK || emin * 0.999999f < refined_bound(p, smin)) amb = vmask;
       }
       // ambiguous lanes (rare) go to the exact fixup kernel (fixup.cuh), which
       // recomputes their pixels' sums and decides them exactly, overwriting
