@@ -540,20 +540,32 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
   p.h = win.h; p.w = win.w; p.l = win.l; p.r = win.r; p.o = win.o; p.u = win.u;
   p.q = q;
   p.n_strips = (int32_t)((W + NT - 1) / NT);
-  int64_t B = 512;
   const int64_t cols = (int64_t)p.n_strips * n_pages;
-  while (B > 4 * (int64_t)win.h && B > 32 && cols * ((H_out + B - 1) / B) < 148 * 4) B /= 2;
+  const size_t smem = quantile_smem_bytes(NT, win.w);
+  if (smem > 48 * 1024) {
+    CK(cudaFuncSetAttribute(k_quantile<NT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    CK(cudaFuncSetAttribute(k_quantile<NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  }
+  // bands: a tile costs its B rows plus h warm-up rows at about half a row
+  // each; minimise waves x tile cost over the resident CTA slots (few tiles
+  // per page: the last wave's tail and the warm-up rows both matter)
+  int per_sm = 0;
+  if (method == ABIN_BERNSEN) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile<NT, 1>, NT, smem));
+  else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile<NT, 0>, NT, smem));
+  const int64_t slots = 148 * (int64_t)std::max(1, per_sm);
+  int64_t B = H_out;
+  double best = 1e300;
+  for (int64_t nb = 1; nb <= std::max<int64_t>(1, H_out / 16); ++nb) {
+    const int64_t Bc = (H_out + nb - 1) / nb;
+    const int64_t waves = (cols * ((H_out + Bc - 1) / Bc) + slots - 1) / slots;
+    const double cost = (double)waves * ((double)Bc + 0.5 * win.h);
+    if (cost < best * 0.999) { best = cost; B = Bc; }
+    if (cols * nb > 64 * slots) break;
+  }
   p.B = (int32_t)B;
   p.n_bands = (int32_t)((H_out + B - 1) / B);
   p.Q_out = Q_out;
-  const size_t smem = quantile_smem_bytes(NT, win.w);
   p.contrast = method == ABIN_BERNSEN ? (int32_t)std::max(-1.0, std::min(256.0, std::floor(q))) : -1;
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_quantile<NT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    CK(cudaFuncSetAttribute(k_quantile<NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
   const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * n_pages;
   if (method == ABIN_BERNSEN) k_quantile<NT, 1><<<(unsigned)n_tiles, NT, smem, st>>>(p);
   else k_quantile<NT, 0><<<(unsigned)n_tiles, NT, smem, st>>>(p);
