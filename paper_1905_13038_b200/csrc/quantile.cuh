@@ -45,6 +45,7 @@ struct QuantParams {
   int32_t B, n_bands, n_strips;
   double* Q_out;  // optional (page 0): Q (Bernsen: the midrange) per pixel as double
   int32_t contrast;  // Bernsen: < 0 plain midrange, else background where max - min < contrast
+  int32_t walk8;     // k_quantile2: rank walks load 8 bins at a time
 };
 
 // A staged pixel's bin code (uint2): x = byte offset of its bin's word in the
@@ -220,6 +221,252 @@ __global__ void __launch_bounds__(NT) k_quantile(const QuantParams p) {
     }
     if (MODE == 0 && p.Q_out && page == 0 && active) p.Q_out[(i - p.row0) * p.W + j] = (double)Qv;
   }
+}
+
+// G = 2 variant of the quantile kernel (MODE 0): thread t owns the two output
+// columns j = J0 + 2t and j + 1.  It keeps the full window histogram of column
+// j and only the difference
+//   Delta = hist(window(j+1)) - hist(window(j)) = col(j+r+1) - col(j-l+1)
+// as biased bytes (128 + Delta, |Delta| <= h <= 127: never carries).  A row
+// step then costs the 2w value updates of window(j) (shared by both pixels)
+// plus four Delta updates, instead of 4w: the recursion of PAPER.md:172
+// shared between neighbouring windows.
+// Layout: the u16 bins of threads t and t + NT/2 share a word (low / high
+// half), the byte deltas of threads t, t + NT/4, ... share a word, so a
+// thread's increments are per-thread constants and a staged pixel's code is
+// just (bin offset, packed compare key).  The rank of each pixel is tracked as
+// in k_quantile (below = #(x < Q)); both pixels' comparisons with (Qa, Qb) come
+// from one subtraction of 16-bit lanes: key = (0x8000 + v) * 0x10001,
+// key - (Qa | Qb << 16) has bit 15 = [v >= Qa] and bit 31 = [v >= Qb], and a
+// sign-replicating byte permute turns them into 0 / 255 lane counters.
+template <int NT>
+__device__ __forceinline__ uint2 bin_code2(uint32_t v) {
+  return make_uint2(v * (uint32_t)(2 * NT), 0x80008000u + v * 0x10001u);
+}
+template <int NT>
+__device__ __forceinline__ uint2 skip_code2() {  // out of the image: trash bin, compares as v = 255 (never < Q)
+  return make_uint2(256u * (uint32_t)(2 * NT), 0x80008000u + 255u * 0x10001u);
+}
+__device__ __forceinline__ uint32_t ge_lanes(uint32_t key, uint32_t qq) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, 0x4B49;" : "=r"(r) : "r"(key - qq));  // bytes 0 / 2 = sign of bytes 1 / 3
+  return r;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
+  extern __shared__ __align__(16) uint8_t qsm[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(qsm);                  // [257][NT/2] u16 pairs (+trash row)
+  uint32_t* dlt = hist + 257 * (NT / 2);                              // [257][NT/4] biased byte quads (+trash)
+  const int span = 2 * NT + p.w;                                      // staged row width
+  uint2* codes = reinterpret_cast<uint2*>(dlt + 257 * (NT / 4));      // [2 buffers][in | out][span]
+
+  const int t = threadIdx.x;
+  int64_t tile = blockIdx.x;
+  const int strip = (int)(tile % p.n_strips);
+  tile /= p.n_strips;
+  const int band = (int)(tile % p.n_bands);
+  const int page = (int)(tile / p.n_bands);
+  const int64_t J0 = (int64_t)strip * 2 * NT;
+  const int64_t j = J0 + 2 * t;           // pixels j (a) and j + 1 (b)
+  const int64_t x0 = J0 - p.l + 1;        // global column of staged element 0
+  const int64_t y0 = p.row0 + (int64_t)band * p.B;
+  const int nrows = (int)min((int64_t)p.B, p.row0 + p.H_out - y0);
+  const uint8_t* img = p.in + (int64_t)page * p.in_page_stride;
+
+  for (int g = t; g < 257 * (NT / 2); g += NT) hist[g] = 0u;
+  for (int g = t; g < 257 * (NT / 4); g += NT) dlt[g] = 0x80808080u;
+
+  const bool act_a = j < p.W, act_b = j + 1 < p.W;
+  const int ncol_a = (int)(min(j + p.r, p.W - 1) - max(j - p.l, (int64_t)-1));
+  const int ncol_b = (int)(min(j + 1 + p.r, p.W - 1) - max(j + 1 - p.l, (int64_t)-1));
+  const int hw_ = t % (NT / 2), hs = 16 * (t / (NT / 2));            // word column / half of my u16 bins
+  const int dw_ = t % (NT / 4), ds = 8 * (t / (NT / 4));             // word column / byte of my deltas
+  const uint32_t hb = static_cast<uint32_t>(__cvta_generic_to_shared(hist + hw_));
+  const uint32_t hd = static_cast<uint32_t>(__cvta_generic_to_shared(dlt + dw_));
+  const uint32_t inc = 1u << hs, dinc = 1u << ds;
+  // window(j) = staged [e0, e0 + w); window(j+1) = [e0 + 1, e0 + w]
+  const int e0 = 2 * t, e1 = 2 * t + p.w;
+
+  constexpr int KS = 4;  // staged elements per thread and row (span <= KS NT: checked at launch)
+  auto fetch = [&](int64_t grow, int (&raw)[KS]) {
+    const bool row_ok = grow >= 0 && grow < p.H_global;
+    const uint8_t* src = img + (grow - p.buf_row0) * p.in_pitch;
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      const int e = t + k * NT;
+      const int64_t col = x0 + e;
+      raw[k] = (e < span && row_ok && col >= 0 && col < p.W) ? (int)__ldg(src + col) : -1;
+    }
+  };
+  auto store_codes = [&](uint2* dst, const int (&raw)[KS]) {
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      const int e = t + k * NT;
+      if (e < span) dst[e] = raw[k] >= 0 ? bin_code2<NT>((uint32_t)raw[k]) : skip_code2<NT>();
+    }
+  };
+  auto atom_add = [](uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+  };
+
+  int Qa = 0, Qb = 0, below_a = 0, below_b = 0;
+  {  // warm-up: rows y0-o .. y0+u-1
+    int raw[KS];
+    fetch(y0 - p.o, raw);
+    for (int64_t a = y0 - p.o; a <= y0 + p.u - 1; ++a) {
+      __syncthreads();
+      store_codes(codes, raw);
+      __syncthreads();
+      if (a + 1 <= y0 + p.u - 1) fetch(a + 1, raw);
+#pragma unroll 4
+      for (int e = e0; e < e1; ++e) atom_add(hb + codes[e].x, inc);
+      atom_add(hd + (codes[e1].x >> 1), dinc);
+      atom_add(hd + (codes[e0].x >> 1), 0u - dinc);
+    }
+  }
+  __syncthreads();
+  uint8_t* orow = p.out + (int64_t)page * p.out_page_stride + (y0 - p.row0) * p.out_pitch;
+  int raw_in[KS], raw_out[KS];
+  int ca_next = 0, cb_next = 0;
+  if (nrows > 0) {
+    fetch(y0 + p.u, raw_in);
+    fetch(y0 - p.o, raw_out);
+    const uint8_t* cr = img + (y0 - p.buf_row0) * p.in_pitch;
+    ca_next = act_a ? (int)__ldg(cr + j) : 0;
+    cb_next = act_b ? (int)__ldg(cr + j + 1) : 0;
+  }
+  auto cnt_a = [&](int g) { return (int)((hist[g * (NT / 2) + hw_] >> hs) & 0xFFFFu); };
+  auto cnt_b = [&](int g) { return cnt_a(g) + (int)((dlt[g * (NT / 4) + dw_] >> ds) & 0xFFu) - 128; };
+  // rank tracking: restore below < rho <= below + cnt(Q).  The counts of 8
+  // bins are loaded at once (independent loads, one latency instead of a
+  // chain): long walks happen where the quantile jumps between the strokes'
+  // and the background's grey levels (q = 0.1 on documents)
+  auto walk1 = [&](int& Q, int& below, int rho, auto cnt) {
+    while (below >= rho) {
+      --Q;
+      below -= cnt(Q);
+    }
+    for (int cq = cnt(Q); below + cq < rho; cq = cnt(Q)) {
+      below += cq;
+      ++Q;
+    }
+  };
+  auto walk = [&](int& Q, int& below, int rho, auto cnt) {
+    if (!p.walk8) {  // (host's choice: long walks are expected for low quantiles on documents)
+      walk1(Q, below, rho, cnt);
+      return;
+    }
+    if (below >= rho) {  // the common short walks: one step at a time first
+      --Q;
+      below -= cnt(Q);
+    }
+    while (below >= rho) {  // down: remove bins Q-1, Q-2, ... while below >= rho
+      int c8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c8[k] = Q - 1 - k >= 0 ? cnt(Q - 1 - k) : 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (below >= rho) { --Q; below -= c8[k]; }
+    }
+    {
+      const int c0 = cnt(Q);
+      if (below + c0 >= rho) return;
+      below += c0;
+      ++Q;
+    }
+    for (;;) {  // up: add bins Q, Q+1, ... while below + cnt(Q) < rho
+      int c8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c8[k] = Q + k <= 255 ? cnt(Q + k) : (1 << 20);
+      bool done = false;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (!done) {
+          if (below + c8[k] < rho) { below += c8[k]; ++Q; }
+          else done = true;
+        }
+      if (done) break;
+    }
+  };
+  for (int qq = 0; qq < nrows; ++qq, orow += p.out_pitch) {
+    const int64_t i = y0 + qq;
+    uint2* c_in = codes + (qq & 1) * 2 * span;
+    uint2* c_out = c_in + span;
+    store_codes(c_in, raw_in);
+    store_codes(c_out, raw_out);
+    const int Ia = ca_next, Ib = cb_next;
+    __syncthreads();
+    if (qq + 1 < nrows) {
+      fetch(i + 1 + p.u, raw_in);
+      fetch(i + 1 - p.o, raw_out);
+      const uint8_t* cr = img + (i + 1 - p.buf_row0) * p.in_pitch;
+      ca_next = act_a ? (int)__ldg(cr + j) : 0;
+      cb_next = act_b ? (int)__ldg(cr + j + 1) : 0;
+    }
+    uint8_t mka = 0, mkb = 0;
+    if (act_a) {
+      const uint32_t qq2 = (uint32_t)Qa | ((uint32_t)Qb << 16);
+      uint32_t acc = 0;  // 16-bit lanes: 255 x (#out >= Q - #in >= Q), |.| <= 255 w < 2^15
+#pragma unroll 4
+      for (int e = e0; e < e1; ++e) {
+        const uint2 a = c_in[e], b = c_out[e];
+        atom_add(hb + a.x, inc);
+        atom_add(hb + b.x, 0u - inc);
+        acc += ge_lanes(b.y, qq2) - ge_lanes(a.y, qq2);
+      }
+      // unpack the signed lanes (acc = lo + 65536 hi mod 2^32)
+      const int lo = (int)(int16_t)(acc & 0xFFFFu);
+      const int hi = (int)(acc - (uint32_t)lo) >> 16;
+      below_a += lo / 255;  // #in < Qa - #out < Qa = #out >= Qa - #in >= Qa
+      below_b += hi / 255;
+      {
+        const uint2 ai = c_in[e1], a0 = c_in[e0], bi = c_out[e1], b0 = c_out[e0];
+        atom_add(hd + (ai.x >> 1), dinc);
+        atom_add(hd + (a0.x >> 1), 0u - dinc);
+        atom_add(hd + (bi.x >> 1), 0u - dinc);
+        atom_add(hd + (b0.x >> 1), dinc);
+        // window(j+1) gains ai, b0 and loses a0, bi: [v < Qb] = 1 - (bit 31 of key - qq2)
+        below_b += (int)((a0.y - qq2) >> 31) + (int)((bi.y - qq2) >> 31) - (int)((ai.y - qq2) >> 31) -
+                   (int)((b0.y - qq2) >> 31);
+      }
+      const int nrow = (int)(min(i + p.u, p.H_global - 1) - max(i - p.o, (int64_t)-1));
+      int rho = (int)ceil(__dmul_rn(p.q, (double)(ncol_a * nrow)));
+      if (rho < 1) rho = 1;
+      walk(Qa, below_a, rho, cnt_a);
+      mka = (Ia <= Qa) ? 0 : 1;
+      if (act_b) {
+        int rb = (int)ceil(__dmul_rn(p.q, (double)(ncol_b * nrow)));
+        if (rb < 1) rb = 1;
+        walk(Qb, below_b, rb, cnt_b);
+        mkb = (Ib <= Qb) ? 0 : 1;
+      }
+    }
+    if (p.fmt == 0) {
+      if (act_a) orow[j] = mka;
+      if (act_b) orow[j + 1] = mkb;
+    } else {
+      // MSB-first bits; lanes 4m .. 4m+3 hold the 8 columns of one byte
+      const unsigned ba = __ballot_sync(0xffffffffu, mka), bb = __ballot_sync(0xffffffffu, mkb);
+      const int lt = t & 31;
+      if ((lt & 3) == 0 && act_a) {
+        uint32_t byte = 0;
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2)
+          byte |= (((ba >> (lt + q2)) & 1u) << (7 - 2 * q2)) | (((bb >> (lt + q2)) & 1u) << (6 - 2 * q2));
+        orow[j >> 3] = (uint8_t)byte;
+      }
+    }
+    if (p.Q_out && page == 0) {
+      if (act_a) p.Q_out[(i - p.row0) * p.W + j] = (double)Qa;
+      if (act_b) p.Q_out[(i - p.row0) * p.W + j + 1] = (double)Qb;
+    }
+  }
+}
+
+inline size_t quantile2_smem_bytes(int nt, int w) {
+  const int span = 2 * nt + w;
+  return (size_t)257 * (nt / 2) * 4 + (size_t)257 * (nt / 4) * 4 + 4 * (size_t)span * 8;
 }
 
 inline size_t quantile_smem_bytes(int nt, int w) {

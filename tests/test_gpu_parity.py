@@ -6,6 +6,7 @@ bit-exact; thresholds (fp64, identical expression order, no contraction)
 within 1e-12 relative -- in practice bit-identical, which is also checked;
 near-ties (|I - t| < 1e-9) counted.
 """
+import functools
 import zlib
 
 import numpy as np
@@ -225,6 +226,43 @@ def test_quantile_small(q):
             assert np.array_equal(mb, oracle.pack_bits(mref))
         s = ab.stats("quantile", to_dev(I), h, w, q)
         assert np.array_equal(s["t"].cpu().numpy(), Qref.astype(np.float64))
+
+
+@pytest.mark.parametrize("single", [False, True])
+@pytest.mark.parametrize("hw", [(3, 3), (12, 7), (51, 51), (125, 40), (126, 40), (30, 128), (30, 129)])
+def test_quantile_both_kernels(monkeypatch, single, hw):
+    """The paired-column kernel (k_quantile2, default where its packing
+    allows: h <= 125, w <= 128) and the single-column kernel (forced with
+    ABIN_QUANTILE_SINGLE, and taken beyond those limits) against the oracle:
+    odd widths (a last thread with one active column), bit masks, a page batch
+    and the Q statistics; windows on both sides of the limits."""
+    if single:
+        monkeypatch.setenv("ABIN_QUANTILE_SINGLE", "1")
+    h, w = hw
+    pages = _quantile_pages()
+    x = torch.from_numpy(pages).to(DEV)
+    for q in (0.5, 0.1):
+        mb = ab.binarize_batched("quantile", x, h, w, q).cpu().numpy()
+        bits = ab.binarize_batched("quantile", x, h, w, q, packed=True).cpu().numpy()
+        for p in range(2):
+            mref, Qref = _quantile_ref(p, h, w, q)
+            assert np.array_equal(mb[p], mref), (hw, q, p)
+            assert np.array_equal(bits[p], oracle.pack_bits(mref)), (hw, q, p)
+        s = ab.stats("quantile", to_dev(pages[1]), h, w, q)
+        assert np.array_equal(s["t"].cpu().numpy(), Qref.astype(np.float64))
+
+
+@functools.lru_cache(maxsize=None)
+def _quantile_pages():
+    rng = np.random.default_rng(5)
+    pages = np.stack([synth.page(120, 261, synth.config_seed(5) + k) for k in range(2)])
+    pages[1, 40:90, 100:200] = rng.integers(0, 256, size=(50, 100), dtype=np.uint8)
+    return pages
+
+
+@functools.lru_cache(maxsize=None)
+def _quantile_ref(p, h, w, q):
+    return oracle.quantile(_quantile_pages()[p], h, w, q)
 
 
 def test_quantile_document_page():
