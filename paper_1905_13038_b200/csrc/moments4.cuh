@@ -119,6 +119,16 @@ __device__ __forceinline__ uint64_t shfl_raw(uint64_t v, int src) {
   return ((uint64_t)hi << 32) | lo;
 }
 
+// sum of the values of lanes lane-1 .. lane-M (wrapped; see the start value)
+template <int M, typename DT>
+__device__ __forceinline__ void lane_sums(uint32_t tc, DT td, int lane, uint32_t& ac, DT& ad) {
+#pragma unroll
+  for (int q = 1; q <= M; ++q) {
+    ac += shfl_raw(tc, lane - q);
+    ad += shfl_raw(td, lane - q);
+  }
+}
+
 // value of lane `src` (0 if src < 0: columns left of the strip are zero)
 __device__ __forceinline__ uint32_t shfl_idx(uint32_t v, int src) {
   const uint32_t r = __shfl_sync(0xffffffffu, v, src & 31);
@@ -390,12 +400,15 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
           // the halo lanes read wrapped-around garbage they never use)
           uint32_t ac = 0u - shfl_raw(sc, lane - mW);
           DT ad = (DT)0 - shfl_raw(sd, lane - mW);
-#pragma unroll
-          for (int q = 1; q <= 8; ++q) {
-            if (q <= mW) {  // warp-uniform: predicated, independent shuffles
-              ac += shfl_raw(tc, lane - q);
-              ad += shfl_raw(td, lane - q);
-            }
+          switch (mW) {  // warp-uniform: one branch, then m independent shuffles
+            case 1: lane_sums<1>(tc, td, lane, ac, ad); break;
+            case 2: lane_sums<2>(tc, td, lane, ac, ad); break;
+            case 3: lane_sums<3>(tc, td, lane, ac, ad); break;
+            case 4: lane_sums<4>(tc, td, lane, ac, ad); break;
+            case 5: lane_sums<5>(tc, td, lane, ac, ad); break;
+            case 6: lane_sums<6>(tc, td, lane, ac, ad); break;
+            case 7: lane_sums<7>(tc, td, lane, ac, ad); break;
+            default: lane_sums<8>(tc, td, lane, ac, ad); break;
           }
           Ac = ac;
           Ad = ad;
