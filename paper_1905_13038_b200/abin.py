@@ -30,6 +30,7 @@ METHODS = {"sauvola": SAUVOLA, "niblack": NIBLACK, "wolf": WOLF, "quantile": QUA
 MASK_U8, MASK_BITS = 0, 1
 FORCE_U64_SQ, FORCE_FP64, HOST_IO, COUNT_STAGES = 1, 2, 4, 8
 V3_INTERNAL = 1 << 29  # internal test hook: the 4-warp-CTA kernel instead of the warp-CTA kernel
+NO_TMA_INTERNAL = 1 << 30  # internal test hook: the generic row loader (no TMA, no re-pitched copy)
 OK, EINVAL, EALIAS, ERANGE, ECUDA, ENOMEM = 0, 1, 2, 3, 4, 5
 
 _lib.abin_sauvola.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _D, _D, _U32, _P, _P]

@@ -119,6 +119,18 @@ def test_generic_loader_equals_tma_path():
     xm.copy_(torch.from_numpy(I).to(DEV))
     c = run("sauvola", xm, 31, 31).cpu().numpy()
     assert np.array_equal(a, b) and np.array_equal(a, c)
+    # unaligned rows are re-pitched for TMA; NO_TMA_INTERNAL keeps the generic loader
+    for x in (to_dev(I, pitch=1000), xm, to_dev(I)):
+        for method in ("sauvola", "niblack", "wolf"):
+            g = run(method, x, 31, 31, flags=abin.NO_TMA_INTERNAL).cpu().numpy()
+            assert np.array_equal(g, run(method, to_dev(I), 31, 31).cpu().numpy()), method
+    # unaligned page batches (page stride 1000 * 200 + 3) through the re-pitch path
+    pb = torch.zeros(3 * (200 * 1000 + 3), dtype=torch.uint8, device=DEV)
+    pages = torch.as_strided(pb, (3, 200, 1000), (200 * 1000 + 3, 1000, 1))
+    pages.copy_(torch.from_numpy(np.stack([I, I[::-1].copy(), 255 - I])).to(DEV))
+    mb = ab.binarize_batched("sauvola", pages, 31, 31, 0.5, 128.0).cpu().numpy()
+    for k, P in enumerate([I, I[::-1].copy(), 255 - I]):
+        assert np.array_equal(mb[k], oracle.binarize("sauvola", P, 31, 31, 0.5, 128.0)), k
 
 
 # ------------------------------------------------------------------ adversarial

@@ -58,3 +58,29 @@ for q in (0.5, 0.1, 0.9):
                       "frac": 2 * 4096 * 4096 / ms / 1e6 / peak}), flush=True)
 ms = timed(lambda k: ab.bernsen(x[k, 0], 51, 51, -1, out=o5[k]), nr, reps=5)
 print(json.dumps({"config": 5, "method": "bernsen", "ms": ms, "gpx_s": 4096 * 4096 / ms / 1e6}), flush=True)
+# config 5b: the 32-page quantile batch
+xb = torch.from_numpy(synth.pages(32, 4096, 4096, synth.config_seed(5), stain=False)).cuda()
+ms = timed(lambda k: ab.binarize_batched("quantile", xb, 51, 51, 0.5), 1, reps=3)
+print(json.dumps({"config": "5b", "method": "quantile q=0.5, 32 pages", "ms": ms, "gpx_s": 32 * 4096 * 4096 / ms / 1e6,
+                  "frac": 2 * 32 * 4096 * 4096 / ms / 1e6 / peak}), flush=True)
+del xb
+# config 1 (one 512^2 page, 32x32, inputs rotated past L2)
+x, nr = pages_dev(1, 512, 512, 1, False)
+o1 = torch.empty((nr, 512, 512), dtype=torch.uint8, device='cuda')
+ms = timed(lambda k: ab.sauvola(x[k, 0], 32, 32, 0.5, 128.0, out=o1[k]), nr, reps=50)
+print(json.dumps({"config": 1, "method": "sauvola", "ms": ms, "gpx_s": 512 * 512 / ms / 1e6}), flush=True)
+# config 4 (32768^2, 101x101, forced u64 square sums, bit mask)
+g = torch.from_numpy(synth.page(32768, 32768, synth.config_seed(4))).cuda()
+ms = timed(lambda k: ab.sauvola(g, 101, 101, 0.34, 128.0, packed=True, flags=abin.FORCE_U64_SQ), 1, reps=5)
+print(json.dumps({"config": 4, "method": "sauvola bits u64", "ms": ms, "gpx_s": 32768 ** 2 / ms / 1e6,
+                  "frac": 1.125 * 32768 ** 2 / ms / 1e6 / peak}), flush=True)
+del g
+# NEXT rows on one config-3 page: Table 1 rules and Otsu
+x, nr = pages_dev(1, 7016, 4960, 3, True)
+RULE_PARAMS = {"feng": (0.85, 0.2, 0.05, 2.0, 64.0), "rais": (), "khurshid": (-0.1, 0),
+               "phansalkar": (0.25, 128.0, 3.0, 10.0 / 255.0)}   # as in tests/test_gpu_parity.py
+for rule in ("feng", "rais", "khurshid", "phansalkar"):
+    ms = timed(lambda k: ab.binarize_rule(rule, x[k, 0], 61, 61, RULE_PARAMS[rule]), nr, reps=5)
+    print(json.dumps({"next": rule, "ms": ms, "gpx_s": 7016 * 4960 / ms / 1e6}), flush=True)
+ms = timed(lambda k: ab.otsu(x[k, 0]), nr, reps=5)
+print(json.dumps({"next": "otsu", "ms": ms, "gpx_s": 7016 * 4960 / ms / 1e6}), flush=True)
