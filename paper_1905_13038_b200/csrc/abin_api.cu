@@ -370,14 +370,10 @@ int run_moments(const MomCall& c) {
   const bool rule = c.method >= ABIN_FENG && c.method <= ABIN_PHANSALKAR;
   const bool stats = c.c_out || c.d_out || c.n_out || c.t_out || c.mask_out;
   // v4 (warp CTAs, certified fp32 + deferred exact fixup) for the production
-  // path; the v3 kernel (inline exact path) for rules, statistics, forced fp64,
-  // rows TMA cannot stage, and bit masks whose 32-bit words are not aligned
-  // (the fixup patches bits with 32-bit atomics)
-  const bool words_ok = c.fmt == ABIN_MASK_U8 ||
-      ((reinterpret_cast<uintptr_t>(c.out) | (uintptr_t)c.out_pitch |
-        (uintptr_t)(c.n_pages > 1 ? c.out_page_stride : 0)) & 3u) == 0;
+  // path; the v3 kernel (inline exact path) for rules, statistics, forced fp64
+  // and rows TMA cannot stage
   const bool use_v4 = fast && tma_ok && !(c.flags & ABIN_V3_INTERNAL) && !rule && !stats &&
-                      !(c.flags & ABIN_FORCE_FP64) && words_ok;
+                      !(c.flags & ABIN_FORCE_FP64);
   CUtensorMap map, map4;
   int rc = encode_map(c, fast ? kR : (nt_wide == 128 ? 8 : 4), tma_ok, &map);
   if (rc == ABIN_OK && use_v4) rc = encode_map_chunks(c, v4::kChunks, v4::kR, &map4);

@@ -165,7 +165,11 @@ static __global__ void __launch_bounds__(kFixNT, 4) k_fixup(const MomParams p) {
       uint8_t* orow = p.out + (int64_t)page * p.out_page_stride + (int64_t)q.y * p.out_pitch;
       if (p.fmt == 0) {
         orow[j] = (uint8_t)mk;
-      } else {  // MSB-first bit j of the row; the word is 4-byte aligned (checked at launch)
+      } else {
+        // MSB-first bit j of the row, patched with a 32-bit atomic on the
+        // aligned word holding its byte (the word's other bytes -- possibly of
+        // a neighbouring row -- are left as they are; CUDA allocations are
+        // 256-byte aligned, so the word never leaves the allocation)
         const uintptr_t addr = reinterpret_cast<uintptr_t>(orow + (j >> 3));
         unsigned int* word = reinterpret_cast<unsigned int*>(addr & ~(uintptr_t)3);
         const unsigned int bit = 1u << (8 * (unsigned)(addr & 3) + (7 - (unsigned)(j & 7)));

@@ -447,20 +447,22 @@ def test_wide_window_kernel():
         check_full(method, I, 8, 1000, packed=True, stats=False)
 
 
+@pytest.mark.parametrize("W", [704, 690])
 @pytest.mark.parametrize("packed", [False, True])
 @pytest.mark.parametrize("cap", [None, 1, 5000])
-def test_fixup_queue_and_overflow(monkeypatch, packed, cap):
+def test_fixup_queue_and_overflow(monkeypatch, packed, cap, W):
     """The v4 kernel queues the pixels its fp32 filter cannot decide; the
     fixup kernel decides them exactly.  On a near-constant page Niblack's
     threshold equals most pixel values (near ties everywhere), so the queue
     holds tens of thousands of pixels: cap=None is the production queue,
     cap=1 / 5000 force the overflow follow-up (the v3 kernel re-does the call
     exactly).  All three: masks bit-exact vs the oracle, near ties counted
-    exactly once."""
+    exactly once.  W = 690: 87-byte bit-mask rows, so the fixup's 32-bit
+    atomics straddle rows."""
     if cap is not None:
         monkeypatch.setenv("ABIN_QUEUE_CAP", str(cap))
     rng = np.random.default_rng(17)
-    P, H, W = 3, 300, 704
+    P, H = 3, 300
     pages = np.full((P, H, W), 128, np.uint8)
     sel = rng.random((P, H, W)) < 2e-4
     pages[sel] = rng.integers(0, 256, int(sel.sum()), dtype=np.uint8)
