@@ -79,6 +79,7 @@ Window effective_window(int32_t h, int32_t w, int64_t Hg, int64_t W) {
 constexpr uint32_t ABIN_NO_TMA_INTERNAL = 1u << 30;
 // internal test hook: the 4-warp-CTA kernel (moments.cuh) instead of the warp-CTA kernel (moments4.cuh)
 constexpr uint32_t ABIN_V3_INTERNAL = 1u << 29;
+constexpr uint32_t ABIN_WIDE_INTERNAL = 1u << 28;  // test hook: the CTA-wide kernel for any window
 constexpr int64_t kMaxDim = (int64_t)1 << 30;
 
 // ---- wide-window fallback (moments_wide.cuh): CTA strips of NT*8 columns
@@ -324,7 +325,7 @@ int run_moments(const MomCall& c) {
   const Window win = effective_window(c.h, c.w, c.H_global, c.W);
   if ((uint64_t)win.h > 66051u) return ABIN_ERANGE;  // column D_j must fit uint32 (255^2 h < 2^32)
   const int KH = (win.w + 1 + kG - 1) / kG;
-  const bool fast = KH <= 31;
+  const bool fast = KH <= 31 && !(c.flags & ABIN_WIDE_INTERNAL);
   const int nt_wide = fast ? 0 : choose_nt_wide(win.w);
   if (!fast && nt_wide == 0) return ABIN_ERANGE;
   // TMA needs a 16-byte aligned base and strides; otherwise the kernels'

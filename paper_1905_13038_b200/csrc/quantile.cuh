@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(NT) k_quantile(const QuantParams p) {
     }
   };
   auto atom_add = [](uint32_t addr, uint32_t v) {
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v));  // no memory clobber: code loads may pass it
   };
 
   int Q = 0, below = 0;  // below = #(x < Q) over the window
@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(NT) k_quantile(const QuantParams p) {
         dbelow += (int)(a.y < qk) - (int)(b.y < qk);
       }
       below += dbelow;
+      asm volatile("" ::: "memory");  // the histogram reads below follow the row's reductions
       } else {
 #pragma unroll 4
         for (int e = s0; e <= s1; ++e) {
@@ -182,6 +183,7 @@ __global__ void __launch_bounds__(NT) k_quantile(const QuantParams p) {
           const int va = (int)(a.y >> 24);
           if (a.y & 0xFFFFFFu) { lo = min(lo, va); hi = max(hi, va); }
         }
+        asm volatile("" ::: "memory");  // the histogram reads below follow the row's reductions
         // removals may have emptied the extreme bins: walk inward (n >= 1)
         while (cnt(lo) == 0) ++lo;
         while (cnt(hi) == 0) --hi;
@@ -234,19 +236,15 @@ __global__ void __launch_bounds__(NT) k_quantile(const QuantParams p) {
 // Layout: the u16 bins of threads t and t + NT/2 share a word (low / high
 // half), the byte deltas of threads t, t + NT/4, ... share a word, so a
 // thread's increments are per-thread constants and a staged pixel's code is
-// just (bin offset, packed compare key).  The rank of each pixel is tracked as
+// just the grey level.  The rank of each pixel is tracked as
 // in k_quantile (below = #(x < Q)); both pixels' comparisons with (Qa, Qb) come
 // from one subtraction of 16-bit lanes: key = (0x8000 + v) * 0x10001,
 // key - (Qa | Qb << 16) has bit 15 = [v >= Qa] and bit 31 = [v >= Qb], and a
 // sign-replicating byte permute turns them into 0 / 255 lane counters.
-template <int NT>
-__device__ __forceinline__ uint2 bin_code2(uint32_t v) {
-  return make_uint2(v * (uint32_t)(2 * NT), 0x80008000u + v * 0x10001u);
-}
-template <int NT>
-__device__ __forceinline__ uint2 skip_code2() {  // out of the image: trash bin, compares as v = 255 (never < Q)
-  return make_uint2(256u * (uint32_t)(2 * NT), 0x80008000u + 255u * 0x10001u);
-}
+// A staged pixel is its grey level v as a u16 code, 256 for pixels outside
+// the image: bin offset code * 2NT (256 = the trash row), compare key
+// (0x8000 + code) * 0x10001 (256 never compares below Q).
+__device__ __forceinline__ uint32_t key2(uint32_t code) { return 0x80008000u + code * 0x10001u; }
 __device__ __forceinline__ uint32_t ge_lanes(uint32_t key, uint32_t qq) {
   uint32_t r;
   asm("prmt.b32 %0, %1, 0, 0x4B49;" : "=r"(r) : "r"(key - qq));  // bytes 0 / 2 = sign of bytes 1 / 3
@@ -259,7 +257,7 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
   uint32_t* hist = reinterpret_cast<uint32_t*>(qsm);                  // [257][NT/2] u16 pairs (+trash row)
   uint32_t* dlt = hist + 257 * (NT / 2);                              // [257][NT/4] biased byte quads (+trash)
   const int span = 2 * NT + p.w;                                      // staged row width
-  uint2* codes = reinterpret_cast<uint2*>(dlt + 257 * (NT / 4));      // [2 buffers][in | out][span]
+  uint16_t* codes = reinterpret_cast<uint16_t*>(dlt + 257 * (NT / 4));  // [2 buffers][in | out][span]
 
   const int t = threadIdx.x;
   int64_t tile = blockIdx.x;
@@ -299,15 +297,16 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
       raw[k] = (e < span && row_ok && col >= 0 && col < p.W) ? (int)__ldg(src + col) : -1;
     }
   };
-  auto store_codes = [&](uint2* dst, const int (&raw)[KS]) {
+  auto store_codes = [&](uint16_t* dst, const int (&raw)[KS]) {
 #pragma unroll
     for (int k = 0; k < KS; ++k) {
       const int e = t + k * NT;
-      if (e < span) dst[e] = raw[k] >= 0 ? bin_code2<NT>((uint32_t)raw[k]) : skip_code2<NT>();
+      if (e < span) dst[e] = (uint16_t)(raw[k] >= 0 ? raw[k] : 256);
     }
   };
+  constexpr uint32_t kRow = 2 * NT;  // bytes per bin row of the u16 bins (NT/2 words); the deltas': NT
   auto atom_add = [](uint32_t addr, uint32_t v) {
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v));  // no memory clobber: code loads may pass it
   };
 
   int Qa = 0, Qb = 0, below_a = 0, below_b = 0;
@@ -320,9 +319,9 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
       __syncthreads();
       if (a + 1 <= y0 + p.u - 1) fetch(a + 1, raw);
 #pragma unroll 4
-      for (int e = e0; e < e1; ++e) atom_add(hb + codes[e].x, inc);
-      atom_add(hd + (codes[e1].x >> 1), dinc);
-      atom_add(hd + (codes[e0].x >> 1), 0u - dinc);
+      for (int e = e0; e < e1; ++e) atom_add(hb + codes[e] * kRow, inc);
+      atom_add(hd + codes[e1] * (uint32_t)NT, dinc);
+      atom_add(hd + codes[e0] * (uint32_t)NT, 0u - dinc);
     }
   }
   __syncthreads();
@@ -391,8 +390,8 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
   };
   for (int qq = 0; qq < nrows; ++qq, orow += p.out_pitch) {
     const int64_t i = y0 + qq;
-    uint2* c_in = codes + (qq & 1) * 2 * span;
-    uint2* c_out = c_in + span;
+    uint16_t* c_in = codes + (qq & 1) * 2 * span;
+    uint16_t* c_out = c_in + span;
     store_codes(c_in, raw_in);
     store_codes(c_out, raw_out);
     const int Ia = ca_next, Ib = cb_next;
@@ -410,10 +409,10 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
       uint32_t acc = 0;  // 16-bit lanes: 255 x (#out >= Q - #in >= Q), |.| <= 255 w < 2^15
 #pragma unroll 4
       for (int e = e0; e < e1; ++e) {
-        const uint2 a = c_in[e], b = c_out[e];
-        atom_add(hb + a.x, inc);
-        atom_add(hb + b.x, 0u - inc);
-        acc += ge_lanes(b.y, qq2) - ge_lanes(a.y, qq2);
+        const uint32_t a = c_in[e], b = c_out[e];
+        atom_add(hb + a * kRow, inc);
+        atom_add(hb + b * kRow, 0u - inc);
+        acc += ge_lanes(key2(b), qq2) - ge_lanes(key2(a), qq2);
       }
       // unpack the signed lanes (acc = lo + 65536 hi mod 2^32)
       const int lo = (int)(int16_t)(acc & 0xFFFFu);
@@ -421,15 +420,16 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
       below_a += lo / 255;  // #in < Qa - #out < Qa = #out >= Qa - #in >= Qa
       below_b += hi / 255;
       {
-        const uint2 ai = c_in[e1], a0 = c_in[e0], bi = c_out[e1], b0 = c_out[e0];
-        atom_add(hd + (ai.x >> 1), dinc);
-        atom_add(hd + (a0.x >> 1), 0u - dinc);
-        atom_add(hd + (bi.x >> 1), 0u - dinc);
-        atom_add(hd + (b0.x >> 1), dinc);
+        const uint32_t ai = c_in[e1], a0 = c_in[e0], bi = c_out[e1], b0 = c_out[e0];
+        atom_add(hd + ai * (uint32_t)NT, dinc);
+        atom_add(hd + a0 * (uint32_t)NT, 0u - dinc);
+        atom_add(hd + bi * (uint32_t)NT, 0u - dinc);
+        atom_add(hd + b0 * (uint32_t)NT, dinc);
         // window(j+1) gains ai, b0 and loses a0, bi: [v < Qb] = 1 - (bit 31 of key - qq2)
-        below_b += (int)((a0.y - qq2) >> 31) + (int)((bi.y - qq2) >> 31) - (int)((ai.y - qq2) >> 31) -
-                   (int)((b0.y - qq2) >> 31);
+        below_b += (int)((key2(a0) - qq2) >> 31) + (int)((key2(bi) - qq2) >> 31) -
+                   (int)((key2(ai) - qq2) >> 31) - (int)((key2(b0) - qq2) >> 31);
       }
+      asm volatile("" ::: "memory");  // the histogram reads below follow the row's reductions
       const int nrow = (int)(min(i + p.u, p.H_global - 1) - max(i - p.o, (int64_t)-1));
       int rho = (int)ceil(__dmul_rn(p.q, (double)(ncol_a * nrow)));
       if (rho < 1) rho = 1;
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
 
 inline size_t quantile2_smem_bytes(int nt, int w) {
   const int span = 2 * nt + w;
-  return (size_t)257 * (nt / 2) * 4 + (size_t)257 * (nt / 4) * 4 + 4 * (size_t)span * 8;
+  return (size_t)257 * (nt / 2) * 4 + (size_t)257 * (nt / 4) * 4 + 4 * (size_t)span * 2;
 }
 
 inline size_t quantile_smem_bytes(int nt, int w) {
