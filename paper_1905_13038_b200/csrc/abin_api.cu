@@ -571,12 +571,12 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
   p.h = win.h; p.w = win.w; p.l = win.l; p.r = win.r; p.o = win.o; p.u = win.u;
   p.q = q;
   // the paired-column kernel (k_quantile2: two outputs per thread sharing one
-  // window histogram) for quantiles whose windows fit its packing and rows it
-  // can stage; Bernsen and the rest take k_quantile
+  // window histogram) for quantiles and Bernsen whose windows fit its packing
+  // and rows it can stage; the rest take k_quantile
   constexpr int NT2 = 64;
   // (shared u16 words: counts + one row's transient adds stay below 2^16;
   // byte deltas 128 + Delta with |Delta| <= h + 2 transiently)
-  const bool pair = method == ABIN_QUANTILE && win.h <= 125 && 2 * NT2 + win.w <= 4 * NT2 &&
+  const bool pair = (method == ABIN_QUANTILE || method == ABIN_BERNSEN) && win.h <= 125 && 2 * NT2 + win.w <= 4 * NT2 &&
                     (int64_t)(win.h + 1) * win.w <= 65535 &&
                     !(getenv("ABIN_QUANTILE_SINGLE"));
   p.n_strips = (int32_t)(pair ? (W + 2 * NT2 - 1) / (2 * NT2) : (W + NT - 1) / NT);
@@ -585,13 +585,14 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
   if (smem > 48 * 1024) {
     CK(cudaFuncSetAttribute(k_quantile<NT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     CK(cudaFuncSetAttribute(k_quantile<NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    CK(cudaFuncSetAttribute(k_quantile2<NT2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    CK(cudaFuncSetAttribute(k_quantile2<NT2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    CK(cudaFuncSetAttribute(k_quantile2<NT2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   }
   // bands: a tile costs its B rows plus h warm-up rows at about half a row
   // each; minimise waves x tile cost over the resident CTA slots (few tiles
   // per page: the last wave's tail and the warm-up rows both matter)
   int per_sm = 0;
-  if (pair) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile2<NT2>, NT2, smem));
+  if (pair) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile2<NT2, 0>, NT2, smem));
   else if (method == ABIN_BERNSEN) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile<NT, 1>, NT, smem));
   else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile<NT, 0>, NT, smem));
   const int64_t slots = 148 * (int64_t)std::max(1, per_sm);
@@ -612,7 +613,8 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
   p.walk8 = (q < 0.25) ? 1 : 0;
   p.contrast = method == ABIN_BERNSEN ? (int32_t)std::max(-1.0, std::min(256.0, std::floor(q))) : -1;
   const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * n_pages;
-  if (pair) k_quantile2<NT2><<<(unsigned)n_tiles, NT2, smem, st>>>(p);
+  if (pair && method == ABIN_BERNSEN) k_quantile2<NT2, 1><<<(unsigned)n_tiles, NT2, smem, st>>>(p);
+  else if (pair) k_quantile2<NT2, 0><<<(unsigned)n_tiles, NT2, smem, st>>>(p);
   else if (method == ABIN_BERNSEN) k_quantile<NT, 1><<<(unsigned)n_tiles, NT, smem, st>>>(p);
   else k_quantile<NT, 0><<<(unsigned)n_tiles, NT, smem, st>>>(p);
   CK(cudaGetLastError());

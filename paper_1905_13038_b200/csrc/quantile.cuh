@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(NT) k_quantile(const QuantParams p) {
   }
 }
 
-// G = 2 variant of the quantile kernel (MODE 0): thread t owns the two output
+// G = 2 variant of the quantile kernel (MODE 0; MODE 1 = Bernsen): thread t owns the two output
 // columns j = J0 + 2t and j + 1.  It keeps the full window histogram of column
 // j and only the difference
 //   Delta = hist(window(j+1)) - hist(window(j)) = col(j+r+1) - col(j-l+1)
@@ -251,7 +251,7 @@ __device__ __forceinline__ uint32_t ge_lanes(uint32_t key, uint32_t qq) {
   return r;
 }
 
-template <int NT>
+template <int NT, int MODE>
 __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
   extern __shared__ __align__(16) uint8_t qsm[];
   uint32_t* hist = reinterpret_cast<uint32_t*>(qsm);                  // [257][NT/2] u16 pairs (+trash row)
@@ -310,6 +310,10 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
   };
 
   int Qa = 0, Qb = 0, below_a = 0, below_b = 0;
+  // MODE 1: bounds on the two windows' extrema (lo <= min, hi >= max); codes
+  // of pixels outside the image (256) never lower a minimum, and as c & 255 = 0
+  // never raise a maximum
+  int lo_a = 255, hi_a = 0, lo_b = 255, hi_b = 0;
   {  // warm-up: rows y0-o .. y0+u-1
     int raw[KS];
     fetch(y0 - p.o, raw);
@@ -318,10 +322,22 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
       store_codes(codes, raw);
       __syncthreads();
       if (a + 1 <= y0 + p.u - 1) fetch(a + 1, raw);
+      uint32_t mn = 256u, mx = 0u;
 #pragma unroll 4
-      for (int e = e0; e < e1; ++e) atom_add(hb + codes[e] * kRow, inc);
+      for (int e = e0; e < e1; ++e) {
+        const uint32_t c = codes[e];
+        atom_add(hb + c * kRow, inc);
+        if (MODE == 1) { mn = min(mn, c); mx = max(mx, c & 255u); }
+      }
       atom_add(hd + codes[e1] * (uint32_t)NT, dinc);
       atom_add(hd + codes[e0] * (uint32_t)NT, 0u - dinc);
+      if (MODE == 1) {
+        const uint32_t ce = codes[e1];
+        lo_a = min(lo_a, (int)mn);
+        hi_a = max(hi_a, (int)mx);
+        lo_b = min(lo_b, (int)min(mn, ce));
+        hi_b = max(hi_b, (int)max(mx, ce & 255u));
+      }
     }
   }
   __syncthreads();
@@ -404,7 +420,36 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
       cb_next = act_b ? (int)__ldg(cr + j + 1) : 0;
     }
     uint8_t mka = 0, mkb = 0;
-    if (act_a) {
+    if (MODE == 1 && act_a) {
+      uint32_t mn = 256u, mx = 0u;
+#pragma unroll 4
+      for (int e = e0; e < e1; ++e) {
+        const uint32_t a = c_in[e], b = c_out[e];
+        atom_add(hb + a * kRow, inc);
+        atom_add(hb + b * kRow, 0u - inc);
+        mn = min(mn, a);
+        mx = max(mx, a & 255u);
+      }
+      const uint32_t ai = c_in[e1], a0 = c_in[e0], bi = c_out[e1], b0 = c_out[e0];
+      atom_add(hd + ai * (uint32_t)NT, dinc);
+      atom_add(hd + a0 * (uint32_t)NT, 0u - dinc);
+      atom_add(hd + bi * (uint32_t)NT, 0u - dinc);
+      atom_add(hd + b0 * (uint32_t)NT, dinc);
+      asm volatile("" ::: "memory");  // the histogram reads below follow the row's reductions
+      lo_a = min(lo_a, (int)mn);
+      hi_a = max(hi_a, (int)mx);
+      lo_b = min(lo_b, (int)min(mn, ai));
+      hi_b = max(hi_b, (int)max(mx, ai & 255u));
+      // removals may have emptied the extreme bins: walk inward (n >= 1)
+      while (cnt_a(lo_a) == 0) ++lo_a;
+      while (cnt_a(hi_a) == 0) --hi_a;
+      mka = (p.contrast >= 0 && hi_a - lo_a < p.contrast) ? 1 : ((2 * Ia <= lo_a + hi_a) ? 0 : 1);
+      if (act_b) {
+        while (cnt_b(lo_b) == 0) ++lo_b;
+        while (cnt_b(hi_b) == 0) --hi_b;
+        mkb = (p.contrast >= 0 && hi_b - lo_b < p.contrast) ? 1 : ((2 * Ib <= lo_b + hi_b) ? 0 : 1);
+      }
+    } else if (MODE == 0 && act_a) {
       const uint32_t qq2 = (uint32_t)Qa | ((uint32_t)Qb << 16);
       uint32_t acc = 0;  // 16-bit lanes: 255 x (#out >= Q - #in >= Q), |.| <= 255 w < 2^15
 #pragma unroll 4
@@ -457,9 +502,9 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
         orow[j >> 3] = (uint8_t)byte;
       }
     }
-    if (p.Q_out && page == 0) {
-      if (act_a) p.Q_out[(i - p.row0) * p.W + j] = (double)Qa;
-      if (act_b) p.Q_out[(i - p.row0) * p.W + j + 1] = (double)Qb;
+    if (p.Q_out && page == 0) {  // Q, or Bernsen's midrange
+      if (act_a) p.Q_out[(i - p.row0) * p.W + j] = MODE == 0 ? (double)Qa : 0.5 * (double)(lo_a + hi_a);
+      if (act_b) p.Q_out[(i - p.row0) * p.W + j + 1] = MODE == 0 ? (double)Qb : 0.5 * (double)(lo_b + hi_b);
     }
   }
 }

@@ -339,10 +339,14 @@ def test_host_io_batched_equals_device_path(packed, pad):
 # ------------------------------------------------------------ Bernsen (NEXT #1)
 
 @pytest.mark.parametrize("contrast", [-1, 15])
-def test_bernsen_small(contrast):
-    """Bernsen midrange on the histogram kernel vs the direct
+@pytest.mark.parametrize("single", [False, True])
+def test_bernsen_small(monkeypatch, contrast, single):
+    """Bernsen midrange on the histogram kernels (the paired
+    k_quantile2 by default, k_quantile with ABIN_QUANTILE_SINGLE) vs the direct
     extrema oracle: random and document images, odd/even windows, windows
     larger than the image, byte and bit masks, tight and padded pitches."""
+    if single:
+        monkeypatch.setenv("ABIN_QUANTILE_SINGLE", "1")
     rng = np.random.default_rng(contrast + 2)
     cases = [((33, 41), (5, 5)), ((64, 200), (51, 51)), ((7, 300), (4, 9)), ((100, 3), (3, 100)),
              ((130, 257), (16, 31))]
