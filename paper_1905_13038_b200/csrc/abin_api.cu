@@ -232,16 +232,22 @@ void choose_bands(int64_t col_tiles, int64_t H_out, int32_t h, int resident, int
 
 // v4 (one warp per CTA, tiles of very different cost at the borders): the
 // makespan is about  total work / slots + one tile  (the last wave's tail),
-// with a tile costing its B rows plus h warm-up rows at about half a row each.
+// with a tile costing its B rows plus h warm-up rows at a fraction wu of a row each.
 // More, shorter bands shrink the tail; the warm-up rows bound how short.
 void choose_bands_v4(int64_t col_tiles, int64_t H_out, int32_t h, int slots, int32_t* B, int32_t* n_bands) {
   double best = 1e300;
   int64_t bestB = H_out;
   const int64_t nb_max = std::max<int64_t>(1, H_out / 16);
+  // weight of a warm-up row (vertical sums only) against an output row, fitted
+  // on the band-count sweeps (tools/band_w.py, tools/sweep.py with ABIN_V4_WU):
+  // 0.3 for single narrow pages (config 2: +10-14 % at h = 127 / 255), 0.5 for
+  // batches and wide pages (config 3 with 16 pages and config 4 lose 1-3 % at 0.3)
+  static const char* wu_env = getenv("ABIN_V4_WU");
+  const double wu = wu_env ? atof(wu_env) : (col_tiles < 32 ? 0.3 : 0.5);
   for (int64_t nb = 1; nb <= nb_max; ++nb) {
     const int64_t Bc = (H_out + nb - 1) / nb;
     const int64_t tiles = col_tiles * ((H_out + Bc - 1) / Bc);
-    const double cost = (double)Bc + 0.5 * h;
+    const double cost = (double)Bc + wu * h;
     const double t = (double)tiles * cost / slots + cost;
     if (t < best * 0.999) { best = t; bestB = Bc; }
   }
