@@ -7,6 +7,10 @@
 namespace abin {
 
 // grid = (blocks_per_page, n_pages); Lw[page] must be initialised to 0xFF.
+#ifndef ABIN_MIN_ROWS
+#define ABIN_MIN_ROWS 2
+#endif
+constexpr int kMinRows = ABIN_MIN_ROWS;  // rows in flight per thread (measured: 2 beats 1, 3, 4 and 8)
 __global__ void __launch_bounds__(256) k_global_min(const uint8_t* __restrict__ in, int64_t page_stride, int64_t H,
                                                     int64_t W, int64_t pitch, unsigned int* Lw) {
   const int page = blockIdx.y;
@@ -15,18 +19,18 @@ __global__ void __launch_bounds__(256) k_global_min(const uint8_t* __restrict__ 
   const bool vec = ((reinterpret_cast<uintptr_t>(img) | (uintptr_t)pitch | (uintptr_t)W) & 15u) == 0;
   if (vec) {
     // rows round-robin over the page's blocks, 16-byte chunks across the
-    // threads; four rows in flight per thread (no per-element division)
+    // threads; kMinRows rows in flight per thread (no per-element division)
     const int64_t wq = W >> 4;  // uint4 per row
-    for (int64_t row = blockIdx.x; row < H; row += 4 * (int64_t)gridDim.x) {
+    for (int64_t row = blockIdx.x; row < H; row += kMinRows * (int64_t)gridDim.x) {
       for (int64_t c = threadIdx.x; c < wq; c += blockDim.x) {
-        uint4 v[4];
+        uint4 v[kMinRows];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kMinRows; ++k) {
           const int64_t rk = row + (int64_t)k * gridDim.x;
           v[k] = rk < H ? __ldg(reinterpret_cast<const uint4*>(img + rk * pitch) + c) : make_uint4(~0u, ~0u, ~0u, ~0u);
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kMinRows; ++k) {
           unsigned int x = __vminu4(__vminu4(v[k].x, v[k].y), __vminu4(v[k].z, v[k].w));
           x = min(min(x & 0xFFu, (x >> 8) & 0xFFu), min((x >> 16) & 0xFFu, x >> 24));
           m = min(m, x);
