@@ -677,12 +677,23 @@ int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8
   const int64_t dpage = dpitch * H, dopage = dopitch * H;
   // chunk of pages per stream and the number of streams in flight (tunable
   // for experiments through ABIN_HOSTIO_CHUNK_MB / ABIN_HOSTIO_STREAMS)
-  static const int64_t chunk_mb = getenv("ABIN_HOSTIO_CHUNK_MB") ? atoll(getenv("ABIN_HOSTIO_CHUNK_MB")) : 64;
-  static const int streams = getenv("ABIN_HOSTIO_STREAMS") ? atoi(getenv("ABIN_HOSTIO_STREAMS")) : 4;
-  int64_t pc = std::max<int64_t>(1, std::min<int64_t>(P, (chunk_mb << 20) / std::max<int64_t>(dpage, 1)));
-  const int nstr = (int)std::min<int64_t>(std::max(1, std::min(streams, (int)HostIoStreams::kMax)), (P + pc - 1) / pc);
+  const int64_t chunk_mb = getenv("ABIN_HOSTIO_CHUNK_MB") ? atoll(getenv("ABIN_HOSTIO_CHUNK_MB")) : 64;
+  const int streams = getenv("ABIN_HOSTIO_STREAMS") ? atoi(getenv("ABIN_HOSTIO_STREAMS")) : 4;
+  const char* cb_env = getenv("ABIN_HOSTIO_CHUNK_BYTES");  // tests: tiny chunks force row bands
+  const int64_t target = cb_env ? std::max<long long>(1, atoll(cb_env)) : (std::max<int64_t>(1, chunk_mb) << 20);
+  // row bands for the methods whose band path needs nothing page-global
+  // (Wolf / Feng only with a given L; the rules' global sums and Otsu never)
+  const bool band_ok = method == ABIN_SAUVOLA || method == ABIN_NIBLACK || method == ABIN_QUANTILE ||
+                       method == ABIN_BERNSEN || ((method == ABIN_WOLF || method == ABIN_FENG) && L >= 0);
+  const int64_t nb = std::min<int64_t>(H, (dpage + target - 1) / target);
+  const bool split = band_ok && nb > 1;
+  const int64_t R = (H + nb - 1) / nb;
+  const int64_t held_max = std::min<int64_t>(H, R + (h + 1) / 2 - 1 + h / 2);
+  int64_t pc = std::max<int64_t>(1, std::min<int64_t>(P, target / std::max<int64_t>(dpage, 1)));
+  const int64_t n_chunks = split ? P * ((H + R - 1) / R) : (P + pc - 1) / pc;
+  const int nstr = (int)std::min<int64_t>(std::max(1, std::min(streams, (int)HostIoStreams::kMax)), n_chunks);
   uint8_t* buf = nullptr;
-  const size_t per = (size_t)(pc * (dpage + dopage));
+  const size_t per = split ? (size_t)(held_max * dpitch + R * dopitch) : (size_t)(pc * (dpage + dopage));
   {
     cudaError_t e = cudaMallocAsync(&buf, per * nstr, st);
     if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? ABIN_ENOMEM : cuda_fail(e);
@@ -693,7 +704,45 @@ int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8
   for (int i = 0; i < nstr; ++i) CK(cudaStreamWaitEvent(hs->s[i], ready, 0));
   const bool contiguous_in = P == 1 || in_page_stride == H * in_pitch;
   const bool contiguous_out = P == 1 || out_page_stride == H * out_pitch;
-  for (int64_t c0 = 0, ci = 0; c0 < P && rc == ABIN_OK; c0 += pc, ++ci) {
+  if (split) {
+    // pages larger than a chunk (a gigapixel scan) travel as row bands with
+    // their window halos (o - 1 rows above, u below; the band path evaluates n
+    // with the page's geometry): device staging stays a few chunks, not pages.
+    // (Smaller chunks for ordinary pages measured slower end to end.)
+    const int64_t o = (h + 1) / 2, u = h / 2;
+    for (int64_t q = 0, ci = 0; q < P && rc == ABIN_OK; ++q) {
+      for (int64_t b = 0; b < nb && rc == ABIN_OK; ++b, ++ci) {
+        const int64_t r0 = b * R, r1 = std::min(H, r0 + R);
+        if (r0 >= r1) break;
+        const int64_t top = std::min(o - 1, r0), bot = std::min(u, H - r1), held = (r1 - r0) + top + bot;
+        cudaStream_t s = hs->s[ci % nstr];
+        uint8_t* din = buf + (ci % nstr) * per;
+        uint8_t* dout = din + held_max * dpitch;
+        const uint8_t* src = in + q * in_page_stride + (r0 - top) * in_pitch;
+        if (in_pitch == dpitch) CK(cudaMemcpyAsync(din, src, (size_t)(held * dpitch), cudaMemcpyHostToDevice, s));
+        else CK(cudaMemcpy2DAsync(din, dpitch, src, in_pitch, W, held, cudaMemcpyHostToDevice, s));
+        if (method == ABIN_QUANTILE || method == ABIN_BERNSEN) {
+          rc = run_quantile(method, din, 0, 1, held, W, dpitch, dout, dopitch, 0, fmt, h, w, p0, r0, r1 - r0, H, held,
+                            r0 - top, s, nullptr);
+        } else {
+          MomCall m;
+          memset(&m, 0, sizeof(m));
+          m.method = method; m.in = din; m.buf_rows = held; m.buf_row0 = r0 - top; m.n_pages = 1;
+          m.W = W; m.in_pitch = dpitch; m.row0 = r0; m.H_out = r1 - r0; m.H_global = H; m.out = dout;
+          m.out_pitch = dopitch; m.fmt = fmt; m.h = h; m.w = w; m.k = p0; m.R = p1; m.L_override = L;
+          m.flags = flags & ~(uint32_t)ABIN_HOST_IO; m.counters = counters; m.stream = s;
+          rc = run_moments(m);
+        }
+        if (rc) break;
+        uint8_t* dst = out + q * out_page_stride + r0 * out_pitch;
+        if (out_pitch == dopitch)
+          CK(cudaMemcpyAsync(dst, dout, (size_t)((r1 - r0) * dopitch), cudaMemcpyDeviceToHost, s));
+        else
+          CK(cudaMemcpy2DAsync(dst, out_pitch, dout, dopitch, orow, r1 - r0, cudaMemcpyDeviceToHost, s));
+      }
+    }
+  }
+  for (int64_t c0 = 0, ci = 0; !split && c0 < P && rc == ABIN_OK; c0 += pc, ++ci) {
     const int64_t np = std::min(pc, P - c0);
     cudaStream_t s = hs->s[ci % nstr];
     uint8_t* din = buf + (ci % nstr) * per;

@@ -95,7 +95,10 @@ __global__ void __launch_bounds__(NT) k_quantile(const QuantParams p) {
   constexpr int KS = 4;
   // raw bytes of global row `grow` for this thread's staged elements (-1: outside the image)
   auto fetch = [&](int64_t grow, int (&raw)[KS]) {
-    const bool row_ok = grow >= 0 && grow < p.H_global;
+    // rows outside the held buffer are never needed for an output: the warm-up
+    // adds row y0 - o and the first step removes it again, and for a band that
+    // row lies above the held halo (o - 1 rows), so both see it as absent
+    const bool row_ok = grow >= 0 && grow < p.H_global && grow >= p.buf_row0 && grow < p.buf_row0 + p.buf_rows;
     const uint8_t* src = img + (grow - p.buf_row0) * p.in_pitch;
 #pragma unroll
     for (int k = 0; k < KS; ++k) {
@@ -288,7 +291,10 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
 
   constexpr int KS = 4;  // staged elements per thread and row (span <= KS NT: checked at launch)
   auto fetch = [&](int64_t grow, int (&raw)[KS]) {
-    const bool row_ok = grow >= 0 && grow < p.H_global;
+    // rows outside the held buffer are never needed for an output: the warm-up
+    // adds row y0 - o and the first step removes it again, and for a band that
+    // row lies above the held halo (o - 1 rows), so both see it as absent
+    const bool row_ok = grow >= 0 && grow < p.H_global && grow >= p.buf_row0 && grow < p.buf_row0 + p.buf_rows;
     const uint8_t* src = img + (grow - p.buf_row0) * p.in_pitch;
 #pragma unroll
     for (int k = 0; k < KS; ++k) {

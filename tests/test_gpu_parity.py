@@ -336,6 +336,43 @@ def test_host_io_batched_equals_device_path(packed, pad):
         assert np.array_equal(got[p], oracle.pack_bits(want) if packed else want), p
 
 
+@pytest.mark.parametrize("method,p0,p1,L", [("sauvola", 0.5, 128.0, -1), ("niblack", -0.2, 0.0, -1),
+                                             ("wolf", 0.5, 128.0, 7), ("quantile", 0.5, 0.0, -1),
+                                             ("bernsen", 15.0, 0.0, -1)])
+@pytest.mark.parametrize("packed,pad", [(False, 0), (True, 3)])
+def test_host_io_row_bands(monkeypatch, method, p0, p1, L, packed, pad):
+    """ABIN_HOST_IO with pages larger than a chunk: each page travels as row
+    bands with their window halos (here ~20 KB chunks: 5 bands per page), and
+    the masks equal the device-resident call's."""
+    monkeypatch.setenv("ABIN_HOSTIO_CHUNK_BYTES", "20000")
+    P, H, W = 3, 230, 333
+    pages = synth.pages(P, H, W, synth.config_seed(3), stain=True)
+    pages[1, 100:140] = 200                                   # flat rows: Niblack ties, fixup queue
+    hbuf = torch.zeros((P, H, W + pad), dtype=torch.uint8).pin_memory()
+    hbuf[:, :, :W] = torch.from_numpy(pages)
+    hin = hbuf[:, :, :W]
+    cols = (W + 7) // 8 if packed else W
+    hout = torch.zeros((P, H, cols + pad), dtype=torch.uint8).pin_memory()
+    fmt = abin.MASK_BITS if packed else abin.MASK_U8
+    rc = abin.raw().abin_binarize_batched(
+        abin.METHODS[method], abin.ctypes.c_void_p(hin.data_ptr()), hin.stride(0),
+        abin.ctypes.c_void_p(hout.data_ptr()), hout.stride(0), P, H, W, hin.stride(1), hout.stride(1), fmt, 31, 25,
+        p0, p1, L, abin.HOST_IO, None, abin.ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    torch.cuda.synchronize()
+    monkeypatch.delenv("ABIN_HOSTIO_CHUNK_BYTES")
+    dev = torch.from_numpy(pages).to(DEV)
+    if method == "wolf":
+        want = ab.binarize_batched(method, dev, 31, 25, p0, p1, L=L, packed=packed)
+    else:
+        want = ab.binarize_batched(method, dev, 31, 25, p0, p1, packed=packed)
+    assert np.array_equal(hout[:, :, :cols].numpy(), want.cpu().numpy())
+    if method == "sauvola":
+        for p in range(P):
+            ref = oracle.binarize("sauvola", pages[p], 31, 25, 0.5, 128.0)
+            assert np.array_equal(want[p].cpu().numpy(), oracle.pack_bits(ref) if packed else ref)
+
+
 # ------------------------------------------------------------ Bernsen (NEXT #1)
 
 @pytest.mark.parametrize("contrast", [-1, 15])
