@@ -467,9 +467,13 @@ int run_moments(const MomCall& c) {
         q.n_bands = (int32_t)((c.H_out + q.B - 1) / q.B);
       }
       // the exact-fixup queue: 16 bytes per ambiguous lane (16 pixels)
-      uint32_t cap = 1u << 20;
+      // at most one entry per output lane-row: calls below the cap cannot
+      // overflow, so they need no follow-up launch and a smaller queue
+      const int64_t max_entries = c.n_pages * c.H_out * ((c.W + 15) / 16 + q.n_strips + 1);
+      uint32_t cap = (uint32_t)std::min<int64_t>(1 << 22, max_entries);  // <= 64 MB: one A4 page at 600 dpi fits
       if (const char* qc = getenv("ABIN_QUEUE_CAP"))  // tests: exercise the overflow follow-up
         cap = (uint32_t)std::max<long long>(1, std::min<long long>(atoll(qc), 1ll << 26));
+      const bool may_overflow = max_entries > (int64_t)cap;
       CK(cudaMallocAsync(&queue, (size_t)cap * 16 + 16, c.stream));
       uint32_t* qcount = reinterpret_cast<uint32_t*>(queue + (size_t)cap);
       CK(cudaMemsetAsync(qcount, 0, 4, c.stream));
@@ -485,6 +489,8 @@ int run_moments(const MomCall& c) {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fixup, kFixNT, fsm));
         k_fixup<<<148 * std::max(1, per_sm), kFixNT, fsm, c.stream>>>(q);
         CK(cudaGetLastError());
+      }
+      if (rc == ABIN_OK && may_overflow) {
         // overflow (pathological inputs only): the v3 kernel redoes the call
         // exactly; its CTAs return at once when the queue held everything
         p.ovf_count = qcount;
