@@ -593,18 +593,24 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
                     !(getenv("ABIN_QUANTILE_SINGLE"));
   p.n_strips = (int32_t)(pair ? (W + 2 * NT2 - 1) / (2 * NT2) : (W + NT - 1) / NT);
   const int64_t cols = (int64_t)p.n_strips * n_pages;
+  // low quantiles of document pages sit where the strokes' grey levels end:
+  // the rank jumps across the empty bins up to the background's, row to row,
+  // so their walks load 8 bins at a time (k_quantile2 MODE 2)
+  const bool groups = pair && method == ABIN_QUANTILE && q < 0.25;
   const size_t smem = pair ? quantile2_smem_bytes(NT2, win.w) : quantile_smem_bytes(NT, win.w);
   if (smem > 48 * 1024) {
     CK(cudaFuncSetAttribute(k_quantile<NT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     CK(cudaFuncSetAttribute(k_quantile<NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     CK(cudaFuncSetAttribute(k_quantile2<NT2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     CK(cudaFuncSetAttribute(k_quantile2<NT2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    CK(cudaFuncSetAttribute(k_quantile2<NT2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   }
   // bands: a tile costs its B rows plus h warm-up rows at about half a row
   // each; minimise waves x tile cost over the resident CTA slots (few tiles
   // per page: the last wave's tail and the warm-up rows both matter)
   int per_sm = 0;
-  if (pair) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile2<NT2, 0>, NT2, smem));
+  if (pair && groups) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile2<NT2, 2>, NT2, smem));
+  else if (pair) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile2<NT2, 0>, NT2, smem));
   else if (method == ABIN_BERNSEN) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile<NT, 1>, NT, smem));
   else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile<NT, 0>, NT, smem));
   const int64_t slots = 148 * (int64_t)std::max(1, per_sm);
@@ -620,12 +626,10 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
   p.B = (int32_t)B;
   p.n_bands = (int32_t)((H_out + B - 1) / B);
   p.Q_out = Q_out;
-  // low quantiles of document pages sit where the strokes' grey levels end:
-  // the rank jumps across the empty bins up to the background's, row to row
-  p.walk8 = (q < 0.25) ? 1 : 0;
   p.contrast = method == ABIN_BERNSEN ? (int32_t)std::max(-1.0, std::min(256.0, std::floor(q))) : -1;
   const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * n_pages;
   if (pair && method == ABIN_BERNSEN) k_quantile2<NT2, 1><<<(unsigned)n_tiles, NT2, smem, st>>>(p);
+  else if (groups) k_quantile2<NT2, 2><<<(unsigned)n_tiles, NT2, smem, st>>>(p);
   else if (pair) k_quantile2<NT2, 0><<<(unsigned)n_tiles, NT2, smem, st>>>(p);
   else if (method == ABIN_BERNSEN) k_quantile<NT, 1><<<(unsigned)n_tiles, NT, smem, st>>>(p);
   else k_quantile<NT, 0><<<(unsigned)n_tiles, NT, smem, st>>>(p);

@@ -45,7 +45,6 @@ struct QuantParams {
   int32_t B, n_bands, n_strips;
   double* Q_out;  // optional (page 0): Q (Bernsen: the midrange) per pixel as double
   int32_t contrast;  // Bernsen: < 0 plain midrange, else background where max - min < contrast
-  int32_t walk8;     // k_quantile2: rank walks load 8 bins at a time
 };
 
 // A staged pixel's bin code (uint2): x = byte offset of its bin's word in the
@@ -337,6 +336,7 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
       }
       atom_add(hd + codes[e1] * (uint32_t)NT, dinc);
       atom_add(hd + codes[e0] * (uint32_t)NT, 0u - dinc);
+
       if (MODE == 1) {
         const uint32_t ce = codes[e1];
         lo_a = min(lo_a, (int)mn);
@@ -359,26 +359,24 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
   }
   auto cnt_a = [&](int g) { return (int)((hist[g * (NT / 2) + hw_] >> hs) & 0xFFFFu); };
   auto cnt_b = [&](int g) { return cnt_a(g) + (int)((dlt[g * (NT / 4) + dw_] >> ds) & 0xFFu) - 128; };
-  // rank tracking: restore below < rho <= below + cnt(Q).  The counts of 8
-  // bins are loaded at once (independent loads, one latency instead of a
-  // chain): long walks happen where the quantile jumps between the strokes'
-  // and the background's grey levels (q = 0.1 on documents)
-  auto walk1 = [&](int& Q, int& below, int rho, auto cnt) {
-    while (below >= rho) {
-      --Q;
-      below -= cnt(Q);
-    }
-    for (int cq = cnt(Q); below + cq < rho; cq = cnt(Q)) {
-      below += cq;
-      ++Q;
-    }
-  };
+  // rank tracking: restore below < rho <= below + cnt(Q).  MODE 2 (low
+  // quantiles: on documents the rank jumps across the empty grey levels
+  // between the strokes' and the background's, row to row) loads the counts
+  // of 8 bins at once once a walk is longer than one step (independent loads,
+  // one latency instead of a chain).  (16-bin group counts measured slower.)
   auto walk = [&](int& Q, int& below, int rho, auto cnt) {
-    if (!p.walk8) {  // (host's choice: long walks are expected for low quantiles on documents)
-      walk1(Q, below, rho, cnt);
+    if (MODE != 2) {
+      while (below >= rho) {
+        --Q;
+        below -= cnt(Q);
+      }
+      for (int cq = cnt(Q); below + cq < rho; cq = cnt(Q)) {
+        below += cq;
+        ++Q;
+      }
       return;
     }
-    if (below >= rho) {  // the common short walks: one step at a time first
+    if (below >= rho) {
       --Q;
       below -= cnt(Q);
     }
@@ -455,7 +453,7 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
         while (cnt_b(hi_b) == 0) --hi_b;
         mkb = (p.contrast >= 0 && hi_b - lo_b < p.contrast) ? 1 : ((2 * Ib <= lo_b + hi_b) ? 0 : 1);
       }
-    } else if (MODE == 0 && act_a) {
+    } else if (MODE != 1 && act_a) {
       const uint32_t qq2 = (uint32_t)Qa | ((uint32_t)Qb << 16);
       uint32_t acc = 0;  // 16-bit lanes: 255 x (#out >= Q - #in >= Q), |.| <= 255 w < 2^15
 #pragma unroll 4
@@ -509,8 +507,8 @@ __global__ void __launch_bounds__(NT) k_quantile2(const QuantParams p) {
       }
     }
     if (p.Q_out && page == 0) {  // Q, or Bernsen's midrange
-      if (act_a) p.Q_out[(i - p.row0) * p.W + j] = MODE == 0 ? (double)Qa : 0.5 * (double)(lo_a + hi_a);
-      if (act_b) p.Q_out[(i - p.row0) * p.W + j + 1] = MODE == 0 ? (double)Qb : 0.5 * (double)(lo_b + hi_b);
+      if (act_a) p.Q_out[(i - p.row0) * p.W + j] = MODE != 1 ? (double)Qa : 0.5 * (double)(lo_a + hi_a);
+      if (act_b) p.Q_out[(i - p.row0) * p.W + j + 1] = MODE != 1 ? (double)Qb : 0.5 * (double)(lo_b + hi_b);
     }
   }
 }
