@@ -36,7 +36,14 @@
  *   When the base, pitch and page stride are multiples of 16 bytes the rows are
  *   staged by TMA in whole 16-byte chunks: the bytes of a row's last partial
  *   chunk (columns W .. ceil(W/16)*16 - 1, inside the pitch) must be readable;
- *   their values are ignored.
+ *   their values are ignored.  Otherwise the moments entry points first copy
+ *   the pages into a 16-byte aligned scratch buffer (one 2-D device copy).
+ * - Scratch: the library takes temporary device memory from the device's
+ *   default stream-ordered pool (cudaMallocAsync) and returns it on the same
+ *   stream: the exact-fixup queue (16 B per output lane-row, at most 64 MB),
+ *   the re-pitched copy above, per-page minima / sums, ABIN_HOST_IO staging.
+ *   It raises the pool's release threshold to 512 MB so that this memory is
+ *   reused across calls instead of re-mapped.
  * - All image / mask pointers are DEVICE pointers (cudaMalloc'd or torch CUDA
  *   tensors) unless the flag ABIN_HOST_IO is given (abin_*_batched only): then
  *   `in` and `out` are HOST pointers (pinned memory recommended) and the
