@@ -89,30 +89,61 @@ def _row_block(t: torch.Tensor) -> torch.Tensor:
     return base
 
 
+class _StagedWork:
+    """gloo with CUDA tensors (functional runs of the multi-rank path on one
+    device): P2P goes through host copies; wait() lands the received rows."""
+
+    def __init__(self, works, landing):
+        self.works, self.landing = works, landing
+
+    def wait(self):
+        for wk in self.works:
+            wk.wait()
+        for dst, src in self.landing:
+            dst.copy_(src)
+
+
 def exchange_halos(band: Band, rank: int, world: int, h: int, group=None):
     """Post the halo exchange (async): send my first u rows up and my last
     o - 1 rows down; receive the rank above's last o - 1 rows into my top halo
     and the rank below's first u rows into my bottom halo.  Returns the works
-    (wait on them before reading the halos)."""
+    (wait on them before reading the halos).  NCCL moves the device rows
+    directly (NVLink P2P); gloo stages device rows through host memory."""
     if world == 1:
         return []
     o, u = window_reach(h)
+    staged = band.own.is_cuda and dist.get_backend(group) == "gloo"
+    landing = []
+
+    def send_buf(t):
+        b = _row_block(t)
+        return b.cpu() if staged else b
+
+    def recv_buf(t):
+        b = _row_block(t)
+        if not staged:
+            return b
+        host = torch.empty(b.shape, dtype=b.dtype)
+        landing.append((b, host))
+        return host
+
     ops = []
     n = band.r1 - band.r0
     own = band.own
     if rank > 0:
         if band.top:
-            ops.append(dist.P2POp(dist.irecv, _row_block(band.halo_top), rank - 1, group))
+            ops.append(dist.P2POp(dist.irecv, recv_buf(band.halo_top), rank - 1, group))
         k = min(u, n)  # the rank above needs min(u, H - its r1) = my first u rows
         if k:
-            ops.append(dist.P2POp(dist.isend, _row_block(own[:k]), rank - 1, group))
+            ops.append(dist.P2POp(dist.isend, send_buf(own[:k]), rank - 1, group))
     if rank < world - 1:
         k = min(o - 1, n)
         if k:
-            ops.append(dist.P2POp(dist.isend, _row_block(own[n - k:]), rank + 1, group))
+            ops.append(dist.P2POp(dist.isend, send_buf(own[n - k:]), rank + 1, group))
         if band.bot:
-            ops.append(dist.P2POp(dist.irecv, _row_block(band.halo_bot), rank + 1, group))
-    return dist.batch_isend_irecv(ops) if ops else []
+            ops.append(dist.P2POp(dist.irecv, recv_buf(band.halo_bot), rank + 1, group))
+    works = dist.batch_isend_irecv(ops) if ops else []
+    return [_StagedWork(works, landing)] if staged else works
 
 
 def run_band(method: str, band: Band, h: int, w: int, param0: float, param1: float = 128.0, L: int = -1,
