@@ -935,7 +935,7 @@ int abin_otsu(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t
   CK(cudaMemsetAsync(hist, 0, 256 * 8, st));
   const unsigned nb = (unsigned)std::min<int64_t>(H, 4 * 148);
   k_otsu_hist<<<dim3(nb, 1), 256, 0, st>>>(in, 0, H, W, in_pitch, hist);
-  k_otsu_pick<<<1, 32, 0, st>>>(hist, t_out ? t_out : tdev, 1, (double)H * (double)W);
+  k_otsu_pick<<<1, 256, 0, st>>>(hist, t_out ? t_out : tdev, 1, (double)H * (double)W);
   k_otsu_mask<<<dim3(nb, 1), 256, 0, st>>>(in, 0, H, W, in_pitch, t_out ? t_out : tdev, out, out_pitch, 0,
                                             mask_format);
   cudaError_t e = cudaGetLastError();

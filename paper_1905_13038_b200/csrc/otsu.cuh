@@ -2,9 +2,9 @@
 // comparator), NEXT #4 of SURVEY section 8(f).
 //   1. k_otsu_hist: exact 256-bin histogram of each page (warp-private
 //      shared-memory sub-histograms, merged with 64-bit global atomics);
-//   2. k_otsu_pick: one thread per page scans t = 0..255 for the maximum of
-//      the between-class variance w0 w1 (mu0 - mu1)^2 in IEEE double, in the
-//      oracle's order (ties keep the smallest t);
+//   2. k_otsu_pick: one block per page, thread t evaluates the between-class
+//      variance w0 w1 (mu0 - mu1)^2 of split t in IEEE double from exact
+//      prefix sums; the argmax keeps the smallest t among ties (the oracle's);
 //   3. k_otsu_mask: I' = 0 iff I <= t (byte or MSB-first bit mask).
 #pragma once
 #include <cstdint>
@@ -44,33 +44,57 @@ static __global__ void __launch_bounds__(256) k_otsu_hist(const uint8_t* __restr
   if (s) atomicAdd(&hist[(int64_t)blockIdx.y * 256 + g], s);
 }
 
-static __global__ void k_otsu_pick(const unsigned long long* hist, uint8_t* t_out, int64_t n_pages, double N) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n_pages) return;
-  const unsigned long long* h = hist + p * 256;
-  unsigned long long Stot = 0;
-  for (int g = 0; g < 256; ++g) Stot += (unsigned long long)g * h[g];
-  const unsigned long long Nt = (unsigned long long)N;
-  unsigned long long N0 = 0, S0 = 0;
-  double best = -1.0;
-  int tbest = 0;
-  for (int t = 0; t < 256; ++t) {
-    N0 += h[t];
-    S0 += (unsigned long long)t * h[t];
-    const unsigned long long N1 = Nt - N0, S1 = Stot - S0;
-    double sb = 0.0;
-    if (N0 > 0 && N1 > 0) {
-      const double w0 = __ddiv_rn((double)N0, N), w1 = __ddiv_rn((double)N1, N);
-      const double mu0 = __ddiv_rn((double)S0, (double)N0), mu1 = __ddiv_rn((double)S1, (double)N1);
-      const double d = __dsub_rn(mu0, mu1);
-      sb = __dmul_rn(__dmul_rn(w0, w1), __dmul_rn(d, d));
-    }
-    if (sb > best) {
-      best = sb;
-      tbest = t;
-    }
+// one 256-thread block per page: thread t evaluates the split t.  N0(t), S0(t)
+// are exact integer prefix sums (a block scan: order-independent), the
+// between-class variance of each t is the oracle's IEEE double sequence, and
+// the block argmax keeps the smallest t among equal maxima -- the oracle's
+// sequential "if (sb > best)" -- so t is bit-identical.
+static __global__ void __launch_bounds__(256) k_otsu_pick(const unsigned long long* hist, uint8_t* t_out,
+                                                          int64_t n_pages, double N) {
+  __shared__ unsigned long long sn[256], ss[256];
+  __shared__ double bsb[8];
+  __shared__ int bt[8];
+  const int64_t p = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const unsigned long long ht = hist[p * 256 + t];
+  sn[t] = ht;
+  ss[t] = (unsigned long long)t * ht;
+  __syncthreads();
+  for (int off = 1; off < 256; off <<= 1) {  // inclusive Hillis-Steele scan
+    const unsigned long long a = t >= off ? sn[t - off] : 0ull, b = t >= off ? ss[t - off] : 0ull;
+    __syncthreads();
+    sn[t] += a;
+    ss[t] += b;
+    __syncthreads();
   }
-  t_out[p] = (uint8_t)tbest;
+  const unsigned long long Nt = sn[255], Stot = ss[255];
+  const unsigned long long N0 = sn[t], S0 = ss[t], N1 = Nt - N0, S1 = Stot - S0;
+  double sb = 0.0;
+  if (N0 > 0 && N1 > 0) {
+    const double w0 = __ddiv_rn((double)N0, N), w1 = __ddiv_rn((double)N1, N);
+    const double mu0 = __ddiv_rn((double)S0, (double)N0), mu1 = __ddiv_rn((double)S1, (double)N1);
+    const double d = __dsub_rn(mu0, mu1);
+    sb = __dmul_rn(__dmul_rn(w0, w1), __dmul_rn(d, d));
+  }
+  // argmax, ties -> smallest t (the sequential scan starts from best = -1, so
+  // t = 0 wins when every sb is 0)
+  double v = sb;
+  int vt = t;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ov = __shfl_down_sync(0xffffffffu, v, off);
+    const int ot = __shfl_down_sync(0xffffffffu, vt, off);
+    if (ov > v || (ov == v && ot < vt)) { v = ov; vt = ot; }
+  }
+  if (lane == 0) { bsb[warp] = v; bt[warp] = vt; }
+  __syncthreads();
+  if (t == 0) {
+    double best = bsb[0];
+    int tb = bt[0];
+    for (int k = 1; k < 8; ++k)
+      if (bsb[k] > best || (bsb[k] == best && bt[k] < tb)) { best = bsb[k]; tb = bt[k]; }
+    t_out[p] = (uint8_t)tb;
+  }
 }
 
 // grid = (blocks_per_page, n_pages); one output byte per pixel (fmt 0) or bit (fmt 1)

@@ -83,3 +83,29 @@ def test_fuzz_quantile_bernsen(seed):
             ref, _, _ = oracle.bernsen(np.ascontiguousarray(pages[p]), h, w, contrast)
             want = oracle.pack_bits(ref) if packed else ref
             assert np.array_equal(got[p], want), (seed, contrast, pages.shape, h, w, pad, packed, p)
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_fuzz_otsu(seed):
+    """Otsu: the block-parallel split scan picks the oracle's t,
+    including ties (two- and three-level images make the between-class
+    variance equal over whole ranges of t: the smallest t must win)."""
+    rng = np.random.default_rng(5000 + seed)
+    H, W = int(rng.integers(1, 300)), int(rng.integers(1, 300))
+    kind = seed % 4
+    if kind == 0:
+        I = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+    elif kind == 1:
+        levels = rng.choice(256, size=int(rng.integers(1, 4)), replace=False).astype(np.uint8)
+        I = levels[rng.integers(0, levels.size, size=(H, W))]
+    elif kind == 2:
+        I = synth.page(max(H, 8), max(W, 8), synth.config_seed(9) + seed, stain=True)
+    else:
+        I = np.clip(rng.normal(128, 40, size=(H, W)), 0, 255).astype(np.uint8)
+    t, ref = oracle.otsu(I)
+    pad = int(rng.choice([0, 3, 16]))
+    buf = torch.zeros((I.shape[0], I.shape[1] + pad), dtype=torch.uint8, device=DEV)
+    buf[:, :I.shape[1]] = torch.from_numpy(np.ascontiguousarray(I)).to(DEV)
+    m, tt = ab.otsu(buf[:, :I.shape[1]])
+    assert int(tt.item()) == t, (seed, kind, I.shape)
+    assert np.array_equal(m.cpu().numpy(), ref)
