@@ -61,8 +61,8 @@ constexpr int kG = 16;                    // columns per lane
 constexpr int kStrip = 32 * kG;           // input columns per warp strip
 constexpr int kChunks = 33;               // TMA box: 33 16-byte chunks = 528 bytes per row
 constexpr int kSpan = 16 * kChunks;       // staged bytes per row (512 + funnel slack)
-constexpr int kR = 2;                     // rows per ring stage (one box per stream)
-constexpr int kNS = 3;                    // ring stages
+constexpr int kR = 3;                     // rows per ring stage (one box per stream; 3 x 2 stages measured best)
+constexpr int kNS = 2;                    // ring stages
 constexpr int kRowsBytes = (kR * kSpan + 127) / 128 * 128;  // one stream of a stage (128-B aligned)
 constexpr int kStageBytes = 2 * kRowsBytes;  // entering + leaving
 
