@@ -239,11 +239,13 @@ void choose_bands_v4(int64_t col_tiles, int64_t H_out, int32_t h, int slots, int
   int64_t bestB = H_out;
   const int64_t nb_max = std::max<int64_t>(1, H_out / 16);
   // weight of a warm-up row (vertical sums only) against an output row, fitted
-  // on the band-count sweeps (tools/band_w.py, tools/sweep.py with ABIN_V4_WU):
-  // 0.3 for single narrow pages (config 2: +10-14 % at h = 127 / 255), 0.5 for
-  // batches and wide pages (config 3 with 16 pages and config 4 lose 1-3 % at 0.3)
+  // on the band-count sweeps (tools/band_w.py, tools/bands.py, tools/abt.py with
+  // ABIN_V4_WU): 0.3 for single narrow pages (config 2: +10-14 % at h = 127 /
+  // 255), 0.5 for small batches and wide pages (16 config-3 pages, config 4),
+  // 0.8 for large batches, whose many waves make warm-up rows count more than
+  // the tail (64 config-3 pages: 699 -> 714 Gpx/s)
   static const char* wu_env = getenv("ABIN_V4_WU");
-  const double wu = wu_env ? atof(wu_env) : (col_tiles < 32 ? 0.3 : 0.5);
+  const double wu = wu_env ? atof(wu_env) : (col_tiles < 32 ? 0.3 : (col_tiles >= 512 ? 0.8 : 0.5));
   for (int64_t nb = 1; nb <= nb_max; ++nb) {
     const int64_t Bc = (H_out + nb - 1) / nb;
     const int64_t tiles = col_tiles * ((H_out + Bc - 1) / Bc);
