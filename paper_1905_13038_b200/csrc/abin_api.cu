@@ -587,7 +587,9 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
   // the paired-column kernel (k_quantile2: two outputs per thread sharing one
   // window histogram) for quantiles and Bernsen whose windows fit its packing
   // and rows it can stage; the rest take k_quantile
-  constexpr int NT2 = 64;
+  // 32 threads (64 columns) per CTA where the window lets a warp stage its
+  // rows (w <= 64: finer tiles, measured 1-10 % faster), else 64
+  const int NT2 = win.w <= 64 ? 32 : 64;
   // (shared u16 words: counts + one row's transient adds stay below 2^16;
   // byte deltas 128 + Delta with |Delta| <= h + 2 transiently)
   const bool pair = (method == ABIN_QUANTILE || method == ABIN_BERNSEN) && win.h <= 125 && 2 * NT2 + win.w <= 4 * NT2 &&
@@ -603,16 +605,25 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
   if (smem > 48 * 1024) {
     CK(cudaFuncSetAttribute(k_quantile<NT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     CK(cudaFuncSetAttribute(k_quantile<NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    CK(cudaFuncSetAttribute(k_quantile2<NT2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    CK(cudaFuncSetAttribute(k_quantile2<NT2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    CK(cudaFuncSetAttribute(k_quantile2<NT2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    for (const void* f : {(const void*)k_quantile2<32, 0>, (const void*)k_quantile2<32, 1>,
+                          (const void*)k_quantile2<32, 2>, (const void*)k_quantile2<64, 0>,
+                          (const void*)k_quantile2<64, 1>, (const void*)k_quantile2<64, 2>})
+      CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  }
+  const int q2_mode = method == ABIN_BERNSEN ? 1 : (groups ? 2 : 0);
+  const void* q2 = nullptr;
+  if (pair) {
+    const void* tab[2][3] = {{(const void*)k_quantile2<32, 0>, (const void*)k_quantile2<32, 1>,
+                              (const void*)k_quantile2<32, 2>},
+                             {(const void*)k_quantile2<64, 0>, (const void*)k_quantile2<64, 1>,
+                              (const void*)k_quantile2<64, 2>}};
+    q2 = tab[NT2 == 64][q2_mode];
   }
   // bands: a tile costs its B rows plus h warm-up rows at about half a row
   // each; minimise waves x tile cost over the resident CTA slots (few tiles
   // per page: the last wave's tail and the warm-up rows both matter)
   int per_sm = 0;
-  if (pair && groups) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile2<NT2, 2>, NT2, smem));
-  else if (pair) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile2<NT2, 0>, NT2, smem));
+  if (pair) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, q2, NT2, smem));
   else if (method == ABIN_BERNSEN) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile<NT, 1>, NT, smem));
   else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile<NT, 0>, NT, smem));
   const int64_t slots = 148 * (int64_t)std::max(1, per_sm);
@@ -630,10 +641,10 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
   p.Q_out = Q_out;
   p.contrast = method == ABIN_BERNSEN ? (int32_t)std::max(-1.0, std::min(256.0, std::floor(q))) : -1;
   const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * n_pages;
-  if (pair && method == ABIN_BERNSEN) k_quantile2<NT2, 1><<<(unsigned)n_tiles, NT2, smem, st>>>(p);
-  else if (groups) k_quantile2<NT2, 2><<<(unsigned)n_tiles, NT2, smem, st>>>(p);
-  else if (pair) k_quantile2<NT2, 0><<<(unsigned)n_tiles, NT2, smem, st>>>(p);
-  else if (method == ABIN_BERNSEN) k_quantile<NT, 1><<<(unsigned)n_tiles, NT, smem, st>>>(p);
+  if (pair) {
+    void* args[] = {&p};
+    CK(cudaLaunchKernel(q2, dim3((unsigned)n_tiles), dim3(NT2), args, smem, st));
+  } else if (method == ABIN_BERNSEN) k_quantile<NT, 1><<<(unsigned)n_tiles, NT, smem, st>>>(p);
   else k_quantile<NT, 0><<<(unsigned)n_tiles, NT, smem, st>>>(p);
   CK(cudaGetLastError());
   return ABIN_OK;
