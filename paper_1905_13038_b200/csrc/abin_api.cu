@@ -629,10 +629,12 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
   const int64_t slots = 148 * (int64_t)std::max(1, per_sm);
   int64_t B = H_out;
   double best = 1e300;
+  static const char* qwu_env = getenv("ABIN_Q_WU");  // experiments: warm-up row weight
+  const double qwu = qwu_env ? atof(qwu_env) : 0.5;
   for (int64_t nb = 1; nb <= std::max<int64_t>(1, H_out / 16); ++nb) {
     const int64_t Bc = (H_out + nb - 1) / nb;
     const int64_t waves = (cols * ((H_out + Bc - 1) / Bc) + slots - 1) / slots;
-    const double cost = (double)waves * ((double)Bc + 0.5 * win.h);
+    const double cost = (double)waves * ((double)Bc + qwu * win.h);
     if (cost < best * 0.999) { best = cost; B = Bc; }
     if (cols * nb > 64 * slots) break;
   }
