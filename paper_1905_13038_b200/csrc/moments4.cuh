@@ -295,7 +295,7 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
     mbar_wait(&full[s % kNS], (s / kNS) & 1);
     const uint8_t* st = ring + (s % kNS) * kStageBytes + eo;
     const int nr = min(2 * kR, p.h - s * 2 * kR);
-#pragma unroll 1
+#pragma unroll 2
     for (int rr = 0; rr < nr; ++rr) {
       const uint8_t* sr = st + (rr < kR ? rr * kSpan : kRowsBytes + (rr - kR) * kSpan);
       const uint4 x = mask_tail(funnel16<DL>(*reinterpret_cast<const uint4*>(sr),
