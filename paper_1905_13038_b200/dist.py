@@ -190,11 +190,15 @@ def run_band(method: str, band: Band, h: int, w: int, param0: float, param1: flo
     return out
 
 
-def global_min_bands(band: Band, group=None) -> int:
+def global_min_bands(band: Band, group=None, local_min=None) -> int:
     """Wolf's L over the whole banded image: per-band minimum, then an
-    all-reduce MIN (one small host read; R8)."""
-    from . import abin
-    L = abin.global_min(band.own).to(torch.int32)
+    all-reduce MIN (one small host read; R8).  `local_min` is the
+    per-band reduction (default: the device kernel abin.global_min; the CPU
+    tests pass a host stand-in to exercise the collective over gloo)."""
+    if local_min is None:
+        from . import abin
+        local_min = abin.global_min
+    L = torch.as_tensor(local_min(band.own)).reshape(1).to(torch.int32)
     if dist.is_available() and dist.is_initialized():
         dist.all_reduce(L, op=dist.ReduceOp.MIN, group=group)
     return int(L.item())

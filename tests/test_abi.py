@@ -90,7 +90,12 @@ def test_band_validation(lib):
     assert args(4, 5) == 1
     assert args(5, 4) == 1
     assert args(5, 5, row0=0) == 1            # halo above the image
-    assert args(0, 5, row0=0, Hg=400) != 1 or True
+    # a first band needs no rows above the image: validation accepts it (with
+    # no CUDA device the first runtime call then fails with ABIN_ECUDA; on a
+    # GPU box the fake pointers must not reach a kernel, so it is not called)
+    import torch
+    if not torch.cuda.is_available():
+        assert args(0, 5, row0=0, Hg=400) == 4
     # Wolf bands need the global L
     assert raw.abin_binarize_band(2, FAKE_IN, 50, 64, 64, 100, 400, 5, 5, FAKE_OUT, 64, 0, 11, 11, 0.5, 128.0, -1,
                                   0, None, None) == 1

@@ -62,13 +62,30 @@ def oracle_band(method, held, row0, H_global, halo_top, halo_bot, h, w, out=None
     return out
 
 
+def _image(H, W, band_L):
+    img = synth.page(H, W, synth.config_seed(4, 7))
+    if band_L:
+        # the page minimum sits in the last band only: the other ranks must
+        # learn it from the all-reduce
+        img[: H - 4] = np.maximum(img[: H - 4], 9)
+        img[H - 2, W // 2] = 0
+    return img
+
+
 def _worker(rank, world, port, H, W, h, w, method, k, R, L, packed, result_path):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        img = synth.page(H, W, synth.config_seed(4, 7))
+        img = _image(H, W, method == "wolf" and L == -1)
         band = adist.make_band(H, W, h, rank, world, device="cpu")
         band.own.copy_(torch.from_numpy(img[band.r0:band.r1]))
+        if method == "wolf":
+            # Wolf's L over the banded image: per-band minimum + all-reduce MIN
+            Lg = adist.global_min_bands(band, local_min=lambda t: t.min())
+            assert Lg == int(img.min())
+            if L != -1:
+                assert L == Lg
+            L = Lg
         out = adist.run_band(method, band, h, w, k, R, L=L, packed=packed, rank=rank, world=world,
                              binarize_band=oracle_band)
         # the halos received must be the true neighbouring rows
@@ -88,17 +105,20 @@ def _worker(rank, world, port, H, W, h, w, method, k, R, L, packed, result_path)
     (2, 37, 29, 9, 7, "sauvola", False),
     (2, 40, 33, 6, 4, "niblack", True),      # even window: asymmetric halos (o - 1 = 2, u = 3)
     (3, 45, 21, 11, 13, "wolf", False),
+    (2, 38, 27, 7, 5, "wolf-bandL", False),   # L from dist.global_min_bands (all-reduce MIN)
     (2, 24, 17, 1, 1, "sauvola", False),     # no halo at all
 ])
 def test_band_decomposition_with_halo_exchange(tmp_path, world, H, W, h, w, method, packed):
+    band_L = method == "wolf-bandL"
+    method = "wolf" if band_L else method
     k, R = {"sauvola": (0.5, 128.0), "niblack": (-0.2, 128.0), "wolf": (0.5, 128.0)}[method]
-    img = synth.page(H, W, synth.config_seed(4, 7))
-    L = oracle.global_min(img) if method == "wolf" else -1
+    img = _image(H, W, band_L)
+    L = oracle.global_min(img) if method == "wolf" and not band_L else -1
     path = str(tmp_path / "mask.npy")
     mp.start_processes(_worker, args=(world, _free_port(), H, W, h, w, method, k, R, L, packed, path),
                        nprocs=world, join=True, start_method="spawn")
     got = np.load(path)
-    want = oracle.binarize(method, img, h, w, k, R, L)
+    want = oracle.binarize(method, img, h, w, k, R, oracle.global_min(img) if method == "wolf" else -1)
     if packed:
         want = oracle.pack_bits(want)
     assert np.array_equal(got, want)

@@ -506,3 +506,147 @@ def test_otsu_invariances():
     assert oracle.otsu((I + 30).astype(np.uint8))[0] == t + 30                 # shift equivariance
     rng = np.random.default_rng(3)
     assert oracle.otsu(rng.permutation(I.ravel()).reshape(60, 50))[0] == t    # only the histogram matters
+
+
+# ------------------------- Table 1 rows evaluated exactly at non-degenerate points
+#
+# The pins above reduce Feng / Rais / Khurshid / Phansalkar to other rules at
+# degenerate parameters (k = 0, p = 0, q = 0, gamma = 0, hw = 1, ms = MS),
+# where a wrong term can vanish.  Here every term is exercised: the window
+# statistics come from a direct Python enumeration of the window's pixels
+# (rows (i-o, i+u], cols (j-l, j+r], pinned above), and the
+# Table 1 row is evaluated in 60-digit Decimal arithmetic,
+# written from the table, not from the oracle.  Each test also checks that
+# the plausible mistakes named in VERDICT (min for max, dropped factor,
+# wrong exponent sign, m (N-1)/N for m^2 (N-1)/N) move t far outside the
+# tolerance, so the pin has teeth.
+
+from decimal import Decimal, getcontext
+
+getcontext().prec = 60
+
+
+def _dec_window(I, h, w, i, j):
+    H, W = I.shape
+    l, r, o, u = (w + 1) // 2, w // 2, (h + 1) // 2, h // 2
+    xs = [int(I[a, b]) for a in range(max(0, i - o + 1), min(H - 1, i + u) + 1)
+          for b in range(max(0, j - l + 1), min(W - 1, j + r) + 1)]
+    n = Decimal(len(xs))
+    m = Decimal(sum(xs)) / n
+    v = Decimal(sum(x * x for x in xs)) / n - m * m
+    return m, v.sqrt(), len(xs)
+
+
+def _dec_global(I):
+    xs = I.astype(np.int64).ravel()
+    N = Decimal(int(xs.size))
+    M = Decimal(int(xs.sum())) / N
+    V = Decimal(int((xs * xs).sum())) / N - M * M
+    return M, V.sqrt()
+
+
+def _pts(H, W, seed, k=40):
+    rng = np.random.default_rng(seed)
+    pts = [(0, 0), (H - 1, W - 1), (0, W - 1), (H // 2, W // 2)]
+    pts += [(int(rng.integers(0, H)), int(rng.integers(0, W))) for _ in range(k)]
+    return pts
+
+
+def _close(a, b, tol=1e-11):
+    return abs(Decimal(a) - b) <= Decimal(tol) * max(Decimal(1), abs(b))
+
+
+def _rule_t(rule, I, h, w, prm, pts):
+    rows = np.array([p[0] for p in pts], np.int64)
+    cols = np.array([p[1] for p in pts], np.int64)
+    return oracle.binarize_rule(rule, I, h, w, prm, rows=rows, cols=cols, with_t=True)
+
+
+def test_rais_exact_off_the_symmetric_point():
+    # t = m + 0.3 (m s - M S) / max{m s, M S} s  (M, S PAPER.md:164-165)
+    I = synth.page(37, 53, synth.config_seed(9, 41), stain=True)
+    h, w = 7, 9
+    M, S = _dec_global(I)
+    pts = _pts(*I.shape, 41)
+    mask, t = _rule_t("rais", I, h, w, (), pts)
+    big = 0
+    for (i, j), tq, mq in zip(pts, t, mask):
+        m, s, _ = _dec_window(I, h, w, i, j)
+        a, b = m * s, M * S
+        exact = m + Decimal("0.3") * (a - b) / max(a, b) * s
+        assert _close(tq, exact), (i, j, tq, exact)
+        assert mq == (0 if Decimal(int(I[i, j])) <= exact else 1) or abs(Decimal(int(I[i, j])) - exact) < Decimal("1e-9")
+        frac = (a - b) / max(a, b)
+        if abs(frac) > Decimal("0.05") and s > 1:
+            big += 1
+            # teeth: min instead of max, a dropped s, 0.3 -> 0.5 all miss by > 1e-3
+            assert abs(m + Decimal("0.3") * (a - b) / min(a, b) * s - exact) > Decimal("1e-3")
+            assert abs(m + Decimal("0.3") * frac - exact) > Decimal("1e-3")
+            assert abs(m + Decimal("0.5") * frac * s - exact) > Decimal("1e-3")
+    assert big >= 10  # the pin exercises the fraction away from 0
+
+
+def test_khurshid_exact_with_the_window_term():
+    # t = m + k sqrt(s^2 + m^2 (hw - 1) / hw): N = h w as printed,
+    # and N = n (the clamped count, SPEC.md:305 flag) at the borders
+    I = synth.page(29, 41, synth.config_seed(9, 42), stain=False)
+    h, w, k = 5, 7, -0.2
+    pts = _pts(*I.shape, 42)
+    teeth = 0
+    for nmode in (0, 1):
+        _, t = _rule_t("khurshid", I, h, w, (k, nmode), pts)
+        for (i, j), tq in zip(pts, t):
+            m, s, n = _dec_window(I, h, w, i, j)
+            N = Decimal(n if nmode else h * w)
+            exact = m + Decimal(k) * (s * s + m * m * (N - 1) / N).sqrt()
+            assert _close(tq, exact), (nmode, i, j, tq, exact)
+            if m > 20:
+                # teeth: m (N-1)/N instead of m^2 (N-1)/N
+                wrong = m + Decimal(k) * (s * s + m * (N - 1) / N).sqrt()
+                assert abs(wrong - exact) > Decimal("1e-3")
+                teeth += 1
+    assert teeth >= 20
+    # the two N modes differ exactly where the window is clipped
+    _, t0 = _rule_t("khurshid", I, h, w, (k, 0), [(0, 0), (14, 20)])
+    _, t1 = _rule_t("khurshid", I, h, w, (k, 1), [(0, 0), (14, 20)])
+    assert t0[0] != t1[0] and t0[1] == t1[1]
+
+
+def test_phansalkar_exact_with_the_exponential():
+    # t = m (1 + p e^{-q m} + k (s/R - 1)), p, q != 0
+    I = synth.page(31, 47, synth.config_seed(9, 43), stain=True)
+    h, w = 9, 9
+    k, R, p, q = 0.25, 128.0, 3.0, 10.0 / 255.0
+    pts = _pts(*I.shape, 43)
+    teeth = 0
+    _, t = _rule_t("phansalkar", I, h, w, (k, R, p, q), pts)
+    for (i, j), tq in zip(pts, t):
+        m, s, _ = _dec_window(I, h, w, i, j)
+        K, Rd, P, Q = (Decimal(x) for x in (k, R, p, q))
+        exact = m * (1 + P * (-Q * m).exp() + K * (s / Rd - 1))
+        assert _close(tq, exact), (i, j, tq, exact)
+        if 5 < m < 150:
+            # teeth: e^{+q m}, e^{-q s}
+            assert abs(m * (1 + P * (Q * m).exp() + K * (s / Rd - 1)) - exact) > Decimal("1e-3")
+            teeth += 1
+            if abs(s - m) > 1:
+                assert abs(m * (1 + P * (-Q * s).exp() + K * (s / Rd - 1)) - exact) > Decimal("1e-3")
+    assert teeth >= 5
+
+
+def test_feng_exact_with_gamma():
+    # t = a1 m + k1 (s/R)^{1+g} (m - L) + k2 (s/R)^g L, L = page min
+    I = synth.page(33, 45, synth.config_seed(9, 44), stain=True)
+    h, w = 7, 7
+    a1, k1, k2, g, R = 0.15, 0.2, 0.03, 2.0, 128.0
+    L = Decimal(int(I.min()))
+    assert L > 0  # the k2 term is exercised
+    pts = _pts(*I.shape, 44)
+    _, t = _rule_t("feng", I, h, w, (a1, k1, k2, g, R), pts)
+    A1, K1, K2, G, Rd = (Decimal(x) for x in (a1, k1, k2, g, R))
+    for (i, j), tq in zip(pts, t):
+        m, s, _ = _dec_window(I, h, w, i, j)
+        x = s / Rd
+        pw = lambda e: Decimal(0) if x == 0 else (e * x.ln()).exp()
+        exact = A1 * m + K1 * pw(1 + G) * (m - L) + K2 * pw(G) * L
+        assert _close(tq, exact, 1e-10), (i, j, tq, exact)
