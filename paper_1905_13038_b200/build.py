@@ -34,16 +34,20 @@ def units():
     return u
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, extra=(), lib: str = LIB, obj: str = OBJ) -> str:
+    """Compile every unit and link `lib`.  `extra` (nvcc flags) and another
+    `lib` / `obj` are for development A/B builds (tools/abbuild.py)."""
     newest = max(os.path.getmtime(s) for s in sources() + [os.path.abspath(__file__)])
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
-        return LIB
-    os.makedirs(OBJ, exist_ok=True)
+    if not force and os.path.exists(lib) and os.path.getmtime(lib) >= newest:
+        return lib
+    os.makedirs(obj, exist_ok=True)
     inc = ["-I", os.path.join(ROOT, "include")]
 
+    obj_dir = obj
+
     def compile_one(unit):
-        obj, src, extra = unit
-        cmd = [NVCC, *NVCC_FLAGS, *extra, *inc, "-c", "-o", os.path.join(OBJ, obj), os.path.join(CSRC, src)]
+        o, src, extra_u = unit
+        cmd = [NVCC, *NVCC_FLAGS, *extra_u, *extra, *inc, "-c", "-o", os.path.join(obj_dir, o), os.path.join(CSRC, src)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -51,16 +55,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed for {src} {extra}:\n{r.stderr}")
         if verbose and r.stderr.strip():
             print(r.stderr, file=sys.stderr)
-        return obj
+        return o
 
     with ThreadPoolExecutor(max_workers=max(1, min(len(units()), os.cpu_count() or 4))) as ex:
         objs = list(ex.map(compile_one, units()))
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *[os.path.join(OBJ, o) for o in objs]]
+    cmd = [NVCC, *ARCH, "-shared", "-o", lib + ".tmp", *[os.path.join(obj_dir, o) for o in objs]]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":

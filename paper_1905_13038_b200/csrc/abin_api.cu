@@ -80,6 +80,7 @@ constexpr uint32_t ABIN_NO_TMA_INTERNAL = 1u << 30;
 // internal test hook: the 4-warp-CTA kernel (moments.cuh) instead of the warp-CTA kernel (moments4.cuh)
 constexpr uint32_t ABIN_V3_INTERNAL = 1u << 29;
 constexpr uint32_t ABIN_WIDE_INTERNAL = 1u << 28;  // test hook: the CTA-wide kernel for any window
+constexpr uint32_t ABIN_V4_INTERNAL = 1u << 27;    // test hook: the v4 warp-CTA kernel instead of v5
 constexpr int64_t kMaxDim = (int64_t)1 << 30;
 
 // ---- wide-window fallback (moments_wide.cuh): CTA strips of NT*8 columns
@@ -118,6 +119,36 @@ int launch_v4_any(int w32, bool d64, const CUtensorMap& map, const MomParams& p,
     case 7: e = launch_v4_part7(w32, d64, map, p, n, st); break;
   }
   return e == cudaSuccess ? ABIN_OK : cuda_fail(e);
+}
+
+int launch_v5_any(int w32, const CUtensorMap& map, const MomParams& p, int64_t n, cudaStream_t st) {
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (w32 >> 2) {
+    case 0: e = launch_v5_part0(w32, map, p, n, st); break;
+    case 1: e = launch_v5_part1(w32, map, p, n, st); break;
+    case 2: e = launch_v5_part2(w32, map, p, n, st); break;
+    case 3: e = launch_v5_part3(w32, map, p, n, st); break;
+    case 4: e = launch_v5_part4(w32, map, p, n, st); break;
+    case 5: e = launch_v5_part5(w32, map, p, n, st); break;
+    case 6: e = launch_v5_part6(w32, map, p, n, st); break;
+    case 7: e = launch_v5_part7(w32, map, p, n, st); break;
+  }
+  return e == cudaSuccess ? ABIN_OK : cuda_fail(e);
+}
+
+// resident v5 warp-CTAs per SM (registers and shared memory, as the runtime reports)
+int occupancy_v5_any(int w32, int method) {
+  switch (w32 >> 2) {
+    case 0: return occupancy_v5_part0(w32, method);
+    case 1: return occupancy_v5_part1(w32, method);
+    case 2: return occupancy_v5_part2(w32, method);
+    case 3: return occupancy_v5_part3(w32, method);
+    case 4: return occupancy_v5_part4(w32, method);
+    case 5: return occupancy_v5_part5(w32, method);
+    case 6: return occupancy_v5_part6(w32, method);
+    case 7: return occupancy_v5_part7(w32, method);
+  }
+  return 16;
 }
 
 int launch_wide_any(bool d64, bool stats, int nt, int ph, const CUtensorMap& map, const wide::MomParams& p,
@@ -170,6 +201,86 @@ FilterConsts filter_consts(int method, double k, double R) {
   f.rdv = (float)(dv * (1 + eps_sqrt) * (1 + 1e-6));
   f.rsdv = (float)(rv * (1 + 1e-6));
   return f;
+}
+
+// Certified bound of the v5 kernel's fp32 residual (moments5.cuh residual2),
+// |e~ - e*| with e* = I - t*, t* the exact threshold of the exact integer
+// sums ("v5 certified bound").  u = 2^-24.  The
+// sequence: m~ = fl(rc nu + Kc), q~ = fl(rd nu + Kd) (Kc = fl(Sc nu),
+// Kd = fl(fl(Sd) nu), rd = fl(rel_d), rc exact, nu = -1/n with relative error
+// e_nu), w~ = fl(m~^2 - q~), s~ = sqrt.approx|w~|, then the Table-1
+// expression.  Counts n lie in [n_min, n_max]; the start value and the
+// relative sums are window sums of windows with counts <= n_max, so they are
+// bounded by 255 n_max (c) and 255^2 n_max (d).
+FilterConsts filter_consts_v5(int method, double k, double R, double n_min, double n_max) {
+  const double u = std::ldexp(1.0, -24);
+  const double eps_sqrt = 8 * u;            // sqrt.approx.f32: relative error < 2^-22 (taken as 2^-21)
+  const double eps64 = 1e-6;                // |t_fp64 - t*| (the canonical double sequence)
+  const double e_nu = 3.01 * u;             // 1/ncol, 1/nrow and their product: three roundings
+  const double ratio = n_max / std::max(1.0, n_min);
+  const double qmax = 255.0 * 255.0, smax = 127.5;
+  const double Mc = 255.0 * ratio;          // bound on |Sc| / n and |rel_c| / n
+  const double dm = 255.0 * (e_nu + 2.01 * u) + 1.01 * Mc * u;                  // |m~ - m|
+  const double dq = qmax * (e_nu + 1.01 * u) + 3.04 * qmax * ratio * u;        // |q~ - q|
+  const double dv = (2 * 255.0 + dm) * dm + dq + 1.01 * u * (smax * smax + 1.0);  // |(-w~) - v|
+  const double rv = std::sqrt(dv);
+  const double ds = rv + eps_sqrt * (smax + rv);                               // |s~ - s| (coarse)
+  FilterConsts f;
+  memset(&f, 0, sizeof(f));
+  auto bound = [&](double dsx) {
+    if (method == M_SAUVOLA) {
+      const double a = std::fabs(1.0 - k), b = std::fabs(k / R);
+      const double G = a + b * (smax + dsx);                                   // |g~|
+      const double dg = b * (dsx + smax * u) + a * u + 1.01 * u * G;           // |g~ - g|
+      return dm * G + 255.0 * dg + dm * dg + 1.01 * u * 255.0 * (1.0 + G);
+    }
+    if (method == M_NIBLACK) {
+      const double ak = std::fabs(k);
+      return dm + 2.02 * u * 255.0 + ak * dsx + ak * smax * u + 1.01 * u * (510.0 + ak * smax);
+    }
+    // Wolf: e = (I - m) + (k (m - L)) (1 - s/R)
+    const double ak = std::fabs(k), iR = 1.0 / R;
+    const double dka = ak * (dm + 255.0 * u) + 2.02 * u * ak * 255.0;           // |ka~ - k (m - L)|
+    const double Bm = 1.0 + (smax + dsx) * iR;                                  // |b~|
+    const double db = dsx * iR + smax * iR * u + 1.01 * u * Bm;                 // |b~ - (1 - s/R)|
+    return dka * Bm + ak * 255.0 * db + dm + 2.02 * u * 255.0 + 1.01 * u * (510.0 + ak * 255.0 * Bm);
+  };
+  if (method == M_SAUVOLA) { f.fa = (float)(1.0 - k); f.fb = (float)(k / R); }
+  else if (method == M_NIBLACK) { f.fa = 0.0f; f.fb = (float)k; }
+  else { f.fa = (float)k; f.fb = (float)(1.0 / R); }
+  f.delta1 = (float)(1.25 * (bound(ds) + eps64) + 1e-6);
+  // data-dependent form (Niblack): |s~ - s| <= min(sqrt dv, dv (1 + eps) / s~) + eps (smax + sqrt dv);
+  // bound(ds) is affine in ds
+  const double b0 = bound(0.0), b1 = bound(1.0) - b0;
+  f.rb0 = (float)((1.25 * (b0 + b1 * eps_sqrt * (smax + rv) + eps64) + 1e-6) * (1 + 1e-6));
+  f.rb1 = (float)(1.25 * b1 * (1 + 1e-6));
+  f.rdv = (float)(dv * (1 + eps_sqrt) * (1 + 1e-6));
+  f.rsdv = (float)(rv * (1 + 1e-6));
+  return f;
+}
+
+// The device's SM count (cudaDevAttrMultiProcessorCount), cached per device;
+// grids and band models are sized in multiples of it.
+int num_sms() {
+  static int cache[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int n = 0;
+    cache[dev] = (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0) ? n : 148;
+  }
+  return cache[dev];
+}
+
+// Resident warp-CTAs per SM of the v4/v5 kernels (launch bounds: 16), as the
+// dynamic shared memory allows (per-SM capacity less the per-block reserve).
+int warp_cta_slots(size_t dyn_smem) {
+  int dev = 0, cap = 0, rsv = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 16;
+  if (cudaDeviceGetAttribute(&cap, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) != cudaSuccess) return 16;
+  if (cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess) rsv = 1024;
+  const int per = (int)(cap / (dyn_smem + (size_t)rsv));
+  return std::max(1, std::min(16, per));
 }
 
 // Validation shared by every entry point.
@@ -395,7 +506,7 @@ int run_moments(const MomCall& c) {
     uint8_t* l8 = reinterpret_cast<uint8_t*>(Lw + c.n_pages);
     k_fill_u32<<<(unsigned)((c.n_pages + 255) / 256), 256, 0, c.stream>>>(Lw, c.n_pages, 0xFFu);
     // pages are whole images here (band mode requires L_override)
-    k_global_min<<<dim3(148, (unsigned)c.n_pages), 256, 0, c.stream>>>(c.in, c.in_page_stride, c.H_out, c.W,
+    k_global_min<<<dim3((unsigned)num_sms(), (unsigned)c.n_pages), 256, 0, c.stream>>>(c.in, c.in_page_stride, c.H_out, c.W,
                                                                          c.in_pitch, Lw);
     k_narrow_u8<<<(unsigned)((c.n_pages + 255) / 256), 256, 0, c.stream>>>(Lw, l8, c.n_pages);
     CK(cudaGetLastError());
@@ -411,7 +522,7 @@ int run_moments(const MomCall& c) {
     CK(cudaMallocAsync(&acc, (size_t)c.n_pages * 32, c.stream));
     CK(cudaMemsetAsync(acc, 0, (size_t)c.n_pages * 16, c.stream));
     double* MS = reinterpret_cast<double*>(acc + 2 * c.n_pages);
-    k_global_sums<<<dim3(148, (unsigned)c.n_pages), 256, 0, c.stream>>>(c.in, c.in_page_stride, c.H_out, c.W,
+    k_global_sums<<<dim3((unsigned)num_sms(), (unsigned)c.n_pages), 256, 0, c.stream>>>(c.in, c.in_page_stride, c.H_out, c.W,
                                                                           c.in_pitch, acc);
     k_mean_std<<<(unsigned)((c.n_pages + 127) / 128), 128, 0, c.stream>>>(acc, MS, c.n_pages,
                                                                             (double)c.H_out * (double)c.W);
@@ -434,7 +545,7 @@ int run_moments(const MomCall& c) {
     p.KH = KH;
     p.Tw = kG * (32 - KH);
     p.n_strips = (int32_t)((c.W + (int64_t)kCW * p.Tw - 1) / ((int64_t)kCW * p.Tw));
-    choose_bands((int64_t)p.n_strips * c.n_pages, c.H_out, win.h, 148 * 4, &p.B, &p.n_bands);
+    choose_bands((int64_t)p.n_strips * c.n_pages, c.H_out, win.h, num_sms() * 4, &p.B, &p.n_bands);
     p.method = c.method;
     p.force_fp64 = ((c.flags & ABIN_FORCE_FP64) || rule) ? 1 : 0;  // rules: every pixel in IEEE double
     p.rp = rp;
@@ -452,6 +563,24 @@ int run_moments(const MomCall& c) {
     const int64_t n_tiles3 = (int64_t)p.n_strips * p.n_bands * c.n_pages;
     if (use_v4) {
       MomParams q = p;
+      // v5 (moments5.cuh) where its exactness conditions hold: biased fp32
+      // column sums need 255^2 h < 2^23, the published row pads ceil(w/16) <= 8
+      // lanes; uint32 square sums (no forced uint64)
+      const bool use_v5 = !d64 && win.h <= v5::kMaxH && win.w <= v5::kMaxW && !(c.flags & ABIN_V4_INTERNAL);
+      if (use_v5) {
+        q.KH = (win.w + kG - 1) / kG;
+        q.Tw = kG * (32 - q.KH);
+        // counts n in [n_min, n_max] for this call: minima at the
+        // first/last column and at the call's first/last output row
+        auto ncol = [&](int64_t j) { return std::min<int64_t>(j + win.r, c.W - 1) - std::max<int64_t>(j - win.l, -1); };
+        auto nrow = [&](int64_t i) { return std::min<int64_t>(i + win.u, c.H_global - 1) - std::max<int64_t>(i - win.o, -1); };
+        const int64_t cmin = std::max<int64_t>(1, std::min(ncol(0), ncol(c.W - 1)));
+        const int64_t rmin = std::max<int64_t>(1, std::min(nrow(c.row0), nrow(c.row0 + c.H_out - 1)));
+        const FilterConsts f5 = filter_consts_v5(c.method, c.k, c.R, (double)(cmin * rmin),
+                                                 (double)win.h * (double)win.w);
+        q.fa = f5.fa; q.fb = f5.fb; q.delta1 = f5.delta1;
+        q.rb0 = f5.rb0; q.rb1 = f5.rb1; q.rdv = f5.rdv; q.rsdv = f5.rsdv;
+      }
       // one warp per CTA; a strip = one warp's 32 - KH valid lanes
       q.n_strips = (int32_t)((c.W + q.Tw - 1) / q.Tw);
       // strips whose windows stay inside [0, W) (ncol = w) are
@@ -462,7 +591,9 @@ int run_moments(const MomCall& c) {
       q.sL = (int32_t)sL;
       q.sR = (int32_t)std::max<int64_t>(sL, std::min<int64_t>(nfit, q.n_strips));
       q.n_pages_v4 = (int32_t)c.n_pages;
-      choose_bands_v4((int64_t)q.n_strips * c.n_pages, c.H_out, win.h, 148 * 16, &q.B, &q.n_bands);
+      choose_bands_v4((int64_t)q.n_strips * c.n_pages, c.H_out, win.h,
+                      num_sms() * (use_v5 ? occupancy_v5_any(win.w % 32, c.method) : warp_cta_slots(v4::smem_bytes())),
+                      &q.B, &q.n_bands);
       if (const char* nb = getenv("ABIN_V4_BANDS")) {  // experiments: force the band count
         const int64_t want = std::max<int64_t>(1, std::min<int64_t>(atoll(nb), c.H_out));
         q.B = (int32_t)((c.H_out + want - 1) / want);
@@ -483,13 +614,13 @@ int run_moments(const MomCall& c) {
       q.q_count = qcount;
       q.q_cap = cap;
       const int64_t n_tiles = (int64_t)q.n_strips * q.n_bands * c.n_pages;
-      rc = launch_v4_any(w32, d64, map4, q, n_tiles, c.stream);
+      rc = use_v5 ? launch_v5_any(w32, map4, q, n_tiles, c.stream) : launch_v4_any(w32, d64, map4, q, n_tiles, c.stream);
       if (rc == ABIN_OK) {
         const size_t fsm = fixup_smem_bytes(win.w);
         if (fsm > 48 * 1024) CK(cudaFuncSetAttribute(k_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
         int per_sm = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fixup, kFixNT, fsm));
-        k_fixup<<<148 * std::max(1, per_sm), kFixNT, fsm, c.stream>>>(q);
+        k_fixup<<<num_sms() * std::max(1, per_sm), kFixNT, fsm, c.stream>>>(q);
         CK(cudaGetLastError());
       }
       if (rc == ABIN_OK && may_overflow) {
@@ -499,7 +630,7 @@ int run_moments(const MomCall& c) {
         p.ovf_cap = cap;
         // about one CTA per SM: the (normal) empty launch costs little
         const int64_t per_band = (int64_t)p.n_strips * c.n_pages;
-        const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(c.H_out, 148 / per_band));
+        const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(c.H_out, num_sms() / per_band));
         p.B = (int32_t)((c.H_out + nb - 1) / nb);
         p.n_bands = (int32_t)((c.H_out + p.B - 1) / p.B);
         rc = launch_fast_any(w32, d64, map, p, per_band * p.n_bands, c.stream);
@@ -519,7 +650,7 @@ int run_moments(const MomCall& c) {
     p.KH = ((win.w + 1 + 8 - 1) / 8 + 1) & ~1;
     p.T = (nt_wide - p.KH - 2) * 8;
     p.n_strips = (int32_t)((c.W + p.T - 1) / p.T);
-    choose_bands((int64_t)p.n_strips * c.n_pages, c.H_out, win.h, 148 * 2, &p.B, &p.n_bands);
+    choose_bands((int64_t)p.n_strips * c.n_pages, c.H_out, win.h, num_sms() * 2, &p.B, &p.n_bands);
     p.method = c.method;
     p.force_fp64 = 1;
     p.rp = rp;
@@ -626,7 +757,7 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
   if (pair) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, q2, NT2, smem));
   else if (method == ABIN_BERNSEN) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile<NT, 1>, NT, smem));
   else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_quantile<NT, 0>, NT, smem));
-  const int64_t slots = 148 * (int64_t)std::max(1, per_sm);
+  const int64_t slots = num_sms() * (int64_t)std::max(1, per_sm);
   int64_t B = H_out;
   double best = 1e300;
   static const char* qwu_env = getenv("ABIN_Q_WU");  // experiments: warm-up row weight
@@ -948,7 +1079,7 @@ int abin_otsu(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t
   CK(cudaMallocAsync(&hist, 256 * 8 + 16, st));
   uint8_t* tdev = reinterpret_cast<uint8_t*>(hist + 256);
   CK(cudaMemsetAsync(hist, 0, 256 * 8, st));
-  const unsigned nb = (unsigned)std::min<int64_t>(H, 4 * 148);
+  const unsigned nb = (unsigned)std::min<int64_t>(H, 4 * num_sms());
   k_otsu_hist<<<dim3(nb, 1), 256, 0, st>>>(in, 0, H, W, in_pitch, hist);
   k_otsu_pick<<<1, 256, 0, st>>>(hist, t_out ? t_out : tdev, 1, (double)H * (double)W);
   k_otsu_mask<<<dim3(nb, 1), 256, 0, st>>>(in, 0, H, W, in_pitch, t_out ? t_out : tdev, out, out_pitch, 0,
@@ -1021,7 +1152,7 @@ int abin_global_min(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, 
   unsigned int* Lw = nullptr;
   CK(cudaMallocAsync(&Lw, (size_t)n_pages * 4, st));
   k_fill_u32<<<(unsigned)((n_pages + 255) / 256), 256, 0, st>>>(Lw, n_pages, 0xFFu);
-  k_global_min<<<dim3(148, (unsigned)n_pages), 256, 0, st>>>(in, in_page_stride, H, W, in_pitch, Lw);
+  k_global_min<<<dim3((unsigned)num_sms(), (unsigned)n_pages), 256, 0, st>>>(in, in_page_stride, H, W, in_pitch, Lw);
   k_narrow_u8<<<(unsigned)((n_pages + 255) / 256), 256, 0, st>>>(Lw, L_out, n_pages);
   cudaError_t e = cudaGetLastError();
   cudaError_t f = cudaFreeAsync(Lw, st);

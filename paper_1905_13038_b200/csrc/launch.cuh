@@ -9,8 +9,23 @@
 #include "moments.cuh"
 #include "moments_wide.cuh"
 #include "moments4.cuh"
+#include "moments5.cuh"
 
 namespace abin {
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, carveout) once per device
+// and kernel (the attributes are per-device state; `done` is the caller's
+// per-kernel static table).  Benign race: the values set are idempotent.
+template <typename K>
+inline cudaError_t set_smem_attr_once(K kern, size_t smem, bool (&done)[64]) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 0 && dev < 64 && done[dev]) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e == cudaSuccess && dev >= 0 && dev < 64) done[dev] = true;
+  return e;
+}
 // warp-strip kernel, w mod 32 = w32 (moments.cuh)
 cudaError_t launch_fast(int w32, bool d64, const CUtensorMap& map, const MomParams& p, int64_t n_tiles,
                         cudaStream_t st);
@@ -23,7 +38,9 @@ cudaError_t launch_wide(bool d64, bool stats, int nt, int ph, const CUtensorMap&
   cudaError_t launch_fast_part##k(int w32, bool d64, const CUtensorMap& map, const MomParams& p, int64_t n, \
                                   cudaStream_t st);                                                         \
   cudaError_t launch_v4_part##k(int w32, bool d64, const CUtensorMap& map, const MomParams& p, int64_t n,   \
-                                cudaStream_t st);
+                                cudaStream_t st);                                                           \
+  cudaError_t launch_v5_part##k(int w32, const CUtensorMap& map, const MomParams& p, int64_t n, cudaStream_t st); \
+  int occupancy_v5_part##k(int w32, int method);
 ABIN_DECL_PART(0) ABIN_DECL_PART(1) ABIN_DECL_PART(2) ABIN_DECL_PART(3)
 ABIN_DECL_PART(4) ABIN_DECL_PART(5) ABIN_DECL_PART(6) ABIN_DECL_PART(7)
 cudaError_t launch_wide_d64(bool d64, bool stats, int nt, int ph, const CUtensorMap& map, const wide::MomParams& p,

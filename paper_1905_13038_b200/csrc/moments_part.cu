@@ -15,13 +15,9 @@ template <int W32, bool D64>
 cudaError_t launch_one(const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st) {
   constexpr size_t smem = moments_smem_bytes();
   auto kern = k_moments<W32, D64>;
-  static bool attr_set = false;  // benign race: the attribute values are idempotent
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static bool attr_set[64] = {};
+  const cudaError_t e = set_smem_attr_once(kern, smem, attr_set);
+  if (e != cudaSuccess) return e;
   kern<<<(unsigned)n_tiles, kNT, smem, st>>>(map, p);
   return cudaGetLastError();
 }
@@ -29,15 +25,48 @@ template <int W32, bool D64, int METHOD>
 cudaError_t launch_v4_m(const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st) {
   constexpr size_t smem = v4::smem_bytes();
   auto kern = v4::k_mom4<W32, D64, METHOD>;
-  static bool attr_set = false;  // benign race: the attribute values are idempotent
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static bool attr_set[64] = {};
+  const cudaError_t e = set_smem_attr_once(kern, smem, attr_set);
+  if (e != cudaSuccess) return e;
   if (n_tiles > 0) kern<<<(unsigned)n_tiles, 32, smem, st>>>(map, p);
   return cudaGetLastError();
+}
+
+template <int W32, int METHOD>
+cudaError_t launch_v5_m(const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st) {
+  constexpr size_t smem = v5::smem_bytes();
+  auto kern = v5::k_mom5<W32, METHOD>;
+  static bool attr_set[64] = {};
+  const cudaError_t e = set_smem_attr_once(kern, smem, attr_set);
+  if (e != cudaSuccess) return e;
+  if (n_tiles > 0) kern<<<(unsigned)n_tiles, 32, smem, st>>>(map, p);
+  return cudaGetLastError();
+}
+
+template <int W32>
+int occ_v5(int method) {
+  int n = 0;
+  constexpr size_t smem = v5::smem_bytes();
+  cudaError_t e;
+  static bool a0[64] = {}, a1[64] = {}, a2[64] = {};
+  if (method == M_SAUVOLA) {
+    e = set_smem_attr_once(v5::k_mom5<W32, M_SAUVOLA>, smem, a0);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, v5::k_mom5<W32, M_SAUVOLA>, 32, smem);
+  } else if (method == M_NIBLACK) {
+    e = set_smem_attr_once(v5::k_mom5<W32, M_NIBLACK>, smem, a1);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, v5::k_mom5<W32, M_NIBLACK>, 32, smem);
+  } else {
+    e = set_smem_attr_once(v5::k_mom5<W32, M_WOLF>, smem, a2);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, v5::k_mom5<W32, M_WOLF>, 32, smem);
+  }
+  return e == cudaSuccess && n > 0 ? n : 16;
+}
+
+template <int W32>
+cudaError_t launch_v5(const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st) {
+  if (p.method == M_SAUVOLA) return launch_v5_m<W32, M_SAUVOLA>(map, p, n_tiles, st);
+  if (p.method == M_NIBLACK) return launch_v5_m<W32, M_NIBLACK>(map, p, n_tiles, st);
+  return launch_v5_m<W32, M_WOLF>(map, p, n_tiles, st);
 }
 
 template <int W32, bool D64>
@@ -58,6 +87,29 @@ cudaError_t ABIN_CAT(launch_v4_part, ABIN_PART)(int w32, bool d64, const CUtenso
     case 3: return d64 ? launch_v4<b + 3, true>(map, p, n, st) : launch_v4<b + 3, false>(map, p, n, st);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t ABIN_CAT(launch_v5_part, ABIN_PART)(int w32, const CUtensorMap& map, const MomParams& p, int64_t n,
+                                                cudaStream_t st) {
+  constexpr int b = 4 * ABIN_PART;
+  switch (w32 - b) {
+    case 0: return launch_v5<b + 0>(map, p, n, st);
+    case 1: return launch_v5<b + 1>(map, p, n, st);
+    case 2: return launch_v5<b + 2>(map, p, n, st);
+    case 3: return launch_v5<b + 3>(map, p, n, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+int ABIN_CAT(occupancy_v5_part, ABIN_PART)(int w32, int method) {
+  constexpr int b = 4 * ABIN_PART;
+  switch (w32 - b) {
+    case 0: return occ_v5<b + 0>(method);
+    case 1: return occ_v5<b + 1>(method);
+    case 2: return occ_v5<b + 2>(method);
+    case 3: return occ_v5<b + 3>(method);
+  }
+  return 16;
 }
 
 cudaError_t ABIN_CAT(launch_fast_part, ABIN_PART)(int w32, bool d64, const CUtensorMap& map, const MomParams& p,

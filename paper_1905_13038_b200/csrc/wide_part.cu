@@ -13,12 +13,9 @@ cudaError_t launch_one(const CUtensorMap& map, const wide::MomParams& p, int64_t
   constexpr int R_ = (NT == 128) ? 8 : 4;
   constexpr size_t smem = wide::moments_smem_bytes<NT, 8, R_, D64>();
   auto kern = wide::k_moments<NT, 8, PH, R_, D64, STATS>;
-  static bool attr_set = false;  // benign race: the attribute value is idempotent
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static bool attr_set[64] = {};  // per device
+  const cudaError_t e = set_smem_attr_once(kern, smem, attr_set);
+  if (e != cudaSuccess) return e;
   kern<<<(unsigned)n_tiles, NT, smem, st>>>(map, p);
   return cudaGetLastError();
 }

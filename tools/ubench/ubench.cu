@@ -48,6 +48,22 @@ __device__ __forceinline__ void step(uint32_t (&a)[NACC], float (&f)[NACC], doub
       asm volatile("add.u32 %0, %0, %1;" : "+r"(a[i]) : "r"(k1));
     }
     if (OP == 23) { asm volatile("add.u32 %0, %0, 1;" : "+r"(a[i])); }
+    if (OP == 24) { f[i] = (float)((a[i] >> 8) & 0xffu); a[i] += __float_as_uint(f[i]); }   // I2F.U8 .B1 (+iadd)
+    if (OP == 25) { float2 x = make_float2(f[i], __uint_as_float(a[i])); x = __ffma2_rn(x, make_float2(__uint_as_float(k1), __uint_as_float(k2)), make_float2(__uint_as_float(k2), __uint_as_float(k1))); f[i] = x.x; a[i] = __float_as_uint(x.y); }  // FFMA2, NACC independent pairs
+    if (OP == 26) { asm volatile("min.f32 %0, %0, %1, %2;" : "+f"(f[i]) : "f"(__uint_as_float(k1)), "f"(__uint_as_float(k2))); }  // FMNMX3
+    if (OP == 27) { asm volatile("cvt.rn.f32.u32 %0, %1;" : "=f"(f[i]) : "r"(a[i])); a[i] += __float_as_uint(f[i]); }  // I2FP.U32 (+iadd)
+    if (OP == 28) { // FFMA2 + IADD3 interleaved
+      float2 x = make_float2(f[i], __uint_as_float(a[(i+4)%NACC])); x = __ffma2_rn(x, make_float2(__uint_as_float(k1), __uint_as_float(k2)), make_float2(__uint_as_float(k2), __uint_as_float(k1))); f[i] = x.x; a[(i+4)%NACC] = __float_as_uint(x.y);
+      asm volatile("add.u32 %0, %0, %1;" : "+r"(a[i]) : "r"(k1));
+    }
+    if (OP == 29) { // FFMA2 + PRMT interleaved
+      float2 x = make_float2(f[i], __uint_as_float(a[(i+4)%NACC])); x = __ffma2_rn(x, make_float2(__uint_as_float(k1), __uint_as_float(k2)), make_float2(__uint_as_float(k2), __uint_as_float(k1))); f[i] = x.x; a[(i+4)%NACC] = __float_as_uint(x.y);
+      asm volatile("prmt.b32 %0, %0, %1, 0x3210;" : "+r"(a[i]) : "r"(k1));
+    }
+    if (OP == 30) { // PRMT + IADD3 interleaved
+      asm volatile("prmt.b32 %0, %0, %1, 0x3210;" : "+r"(a[i]) : "r"(k1));
+      asm volatile("add.u32 %0, %0, %1;" : "+r"(a[(i+4)%NACC]) : "r"(k2));
+    }
   }
 }
 
@@ -114,5 +130,12 @@ int main() {
   run<15>("IADD3+IMAD pair (ops)", 2, nsm, b);
   run<16>("PRMT+IDP.2A pair (ops)", 2, nsm, b);
   run<22>("MUFU.SQRT+IADD pair (ops)", 2, nsm, b);
+  run<24>("I2F.U8.B1 + IADD (pair)", 2, nsm, b);
+  run<25>("FFMA2 (instr)", 1, nsm, b);
+  run<26>("FMNMX3", 1, nsm, b);
+  run<27>("I2FP.U32 + IADD (pair)", 2, nsm, b);
+  run<28>("FFMA2+IADD3 pair (instr)", 2, nsm, b);
+  run<29>("FFMA2+PRMT pair (instr)", 2, nsm, b);
+  run<30>("PRMT+IADD3 pair (instr)", 2, nsm, b);
   return 0;
 }
