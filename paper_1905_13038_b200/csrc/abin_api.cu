@@ -82,6 +82,7 @@ constexpr uint32_t ABIN_V3_INTERNAL = 1u << 29;
 constexpr uint32_t ABIN_WIDE_INTERNAL = 1u << 28;  // test hook: the CTA-wide kernel for any window
 constexpr uint32_t ABIN_V4_INTERNAL = 1u << 27;    // test hook: the v4 warp-CTA kernel instead of v5
 constexpr int64_t kMaxDim = (int64_t)1 << 30;
+constexpr int kQuantNT = 128;  // threads of the single-column quantile kernel (its staging bounds w)
 
 // ---- wide-window fallback (moments_wide.cuh): CTA strips of NT*8 columns
 int choose_nt_wide(int32_t w_eff) {
@@ -678,13 +679,16 @@ int run_moments(const MomCall& c) {
   return rc;
 }
 
+// Parameters of the batched / band / stats entry points: methods 0..4 (the
+// Table-1 rules 5..8 take their own parameter array through
+// abin_binarize_rule; these entry points have no place for it).
 int check_params(int32_t method, double p0, double p1) {
+  if (method < ABIN_SAUVOLA || method > ABIN_BERNSEN) return ABIN_EINVAL;
   if (method == ABIN_QUANTILE) return (std::isfinite(p0) && p0 > 0.0 && p0 <= 1.0) ? ABIN_OK : ABIN_EINVAL;
   if (method == ABIN_BERNSEN) return std::isfinite(p0) ? ABIN_OK : ABIN_EINVAL;  // contrast (< 0: plain midrange)
   if (!std::isfinite(p0)) return ABIN_EINVAL;
   if (method == ABIN_SAUVOLA || method == ABIN_WOLF)
     if (!std::isfinite(p1) || !(p1 > 0.0)) return ABIN_EINVAL;
-  if (method < 0 || method > 8) return ABIN_EINVAL;
   return ABIN_OK;
 }
 
@@ -694,7 +698,7 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
                  int32_t w, double q, int64_t row0, int64_t H_out, int64_t H_global, int64_t buf_rows,
                  int64_t buf_row0, cudaStream_t st, double* Q_out) {
   const Window win = effective_window(h, w, H_global, W);
-  constexpr int NT_ = 128;
+  constexpr int NT_ = kQuantNT;
   if ((int64_t)win.h * win.w > 65535) return ABIN_ERANGE;  // u16 bins
   if (NT_ + win.w - 1 > 4 * NT_) return ABIN_ERANGE;  // a thread stages at most 4 elements of a row
   constexpr int NT = 128;
@@ -820,6 +824,32 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
                  int32_t w, double q, int64_t row0, int64_t H_out, int64_t H_global, int64_t buf_rows,
                  int64_t buf_row0, cudaStream_t st, double* Q_out);
 
+// Host <-> device copies of `rows` rows of `width` bytes.  Only the caller's
+// `width` bytes per row are read or written (the padding of a row and the
+// bytes past the last row belong to the caller): a single linear DMA when the
+// rows are contiguous (pitch == width), else all rows but the last as one
+// linear copy of whole pitches (host input only: reading a row's padding is
+// harmless, the next row follows it) plus the last row, else a 2-D copy.
+cudaError_t copy_rows_h2d(uint8_t* dst, int64_t dpitch, const uint8_t* src, int64_t spitch, int64_t width,
+                          int64_t rows, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  if (spitch == dpitch) {
+    cudaError_t e = cudaSuccess;
+    if (rows > 1) e = cudaMemcpyAsync(dst, src, (size_t)((rows - 1) * spitch), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(dst + (rows - 1) * dpitch, src + (rows - 1) * spitch, (size_t)width, cudaMemcpyHostToDevice, s);
+    return e;
+  }
+  return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyHostToDevice, s);
+}
+cudaError_t copy_rows_d2h(uint8_t* dst, int64_t dpitch, const uint8_t* src, int64_t spitch, int64_t width,
+                          int64_t rows, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  if (dpitch == width && spitch == width)
+    return cudaMemcpyAsync(dst, src, (size_t)(rows * width), cudaMemcpyDeviceToHost, s);
+  return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToHost, s);
+}
+
 int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8_t* out, int64_t out_page_stride,
                 int64_t P, int64_t H, int64_t W, int64_t in_pitch, int64_t out_pitch, int32_t fmt, int32_t h,
                 int32_t w, double p0, double p1, int32_t L, uint32_t flags, uint64_t* counters, cudaStream_t st) {
@@ -829,7 +859,9 @@ int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8
   // device staging keeps the host pitch when it is TMA-friendly, so the copies are linear
   const int64_t dpitch = (in_pitch % 16 == 0) ? in_pitch : (W + 15) / 16 * 16;
   const int64_t orow = fmt == ABIN_MASK_U8 ? W : (W + 7) / 8;
-  const int64_t dopitch = (out_pitch % 16 == 0) ? out_pitch : (orow + 15) / 16 * 16;
+  // the staged mask rows are tight (row bytes) when the caller's are: one
+  // linear D2H copy; otherwise the caller's pitch (a 2-D copy of the row bytes)
+  const int64_t dopitch = out_pitch == orow ? orow : ((out_pitch % 16 == 0) ? out_pitch : (orow + 15) / 16 * 16);
   const int64_t dpage = dpitch * H, dopage = dopitch * H;
   // chunk of pages per stream and the number of streams in flight (tunable
   // for experiments through ABIN_HOSTIO_CHUNK_MB / ABIN_HOSTIO_STREAMS)
@@ -875,8 +907,7 @@ int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8
         uint8_t* din = buf + (ci % nstr) * per;
         uint8_t* dout = din + held_max * dpitch;
         const uint8_t* src = in + q * in_page_stride + (r0 - top) * in_pitch;
-        if (in_pitch == dpitch) CK(cudaMemcpyAsync(din, src, (size_t)(held * dpitch), cudaMemcpyHostToDevice, s));
-        else CK(cudaMemcpy2DAsync(din, dpitch, src, in_pitch, W, held, cudaMemcpyHostToDevice, s));
+        CK(copy_rows_h2d(din, dpitch, src, in_pitch, W, held, s));
         if (method == ABIN_QUANTILE || method == ABIN_BERNSEN) {
           rc = run_quantile(method, din, 0, 1, held, W, dpitch, dout, dopitch, 0, fmt, h, w, p0, r0, r1 - r0, H, held,
                             r0 - top, s, nullptr);
@@ -890,11 +921,7 @@ int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8
           rc = run_moments(m);
         }
         if (rc) break;
-        uint8_t* dst = out + q * out_page_stride + r0 * out_pitch;
-        if (out_pitch == dopitch)
-          CK(cudaMemcpyAsync(dst, dout, (size_t)((r1 - r0) * dopitch), cudaMemcpyDeviceToHost, s));
-        else
-          CK(cudaMemcpy2DAsync(dst, out_pitch, dout, dopitch, orow, r1 - r0, cudaMemcpyDeviceToHost, s));
+        CK(copy_rows_d2h(out + q * out_page_stride + r0 * out_pitch, out_pitch, dout, dopitch, orow, r1 - r0, s));
       }
     }
   }
@@ -903,14 +930,11 @@ int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8
     cudaStream_t s = hs->s[ci % nstr];
     uint8_t* din = buf + (ci % nstr) * per;
     uint8_t* dout = din + pc * dpage;
-    if (contiguous_in && in_pitch == dpitch) {  // one linear DMA (2-D copies run at about half the PCIe rate)
-      CK(cudaMemcpyAsync(din, in + c0 * in_page_stride, (size_t)(np * H * dpitch), cudaMemcpyHostToDevice, s));
-    } else if (contiguous_in) {
-      CK(cudaMemcpy2DAsync(din, dpitch, in + c0 * in_page_stride, in_pitch, W, np * H, cudaMemcpyHostToDevice, s));
+    // linear DMAs where the layout allows (2-D copies run at about half the PCIe rate)
+    if (contiguous_in) {
+      CK(copy_rows_h2d(din, dpitch, in + c0 * in_page_stride, in_pitch, W, np * H, s));
     } else {
-      for (int64_t q = 0; q < np; ++q)
-        CK(cudaMemcpy2DAsync(din + q * dpage, dpitch, in + (c0 + q) * in_page_stride, in_pitch, W, H,
-                             cudaMemcpyHostToDevice, s));
+      for (int64_t q = 0; q < np; ++q) CK(copy_rows_h2d(din + q * dpage, dpitch, in + (c0 + q) * in_page_stride, in_pitch, W, H, s));
     }
     if (method == ABIN_QUANTILE || method == ABIN_BERNSEN) {
       rc = run_quantile(method, din, dpage, np, H, W, dpitch, dout, dopitch, dopage, fmt, h, w, p0, 0, H, H, H, 0, s, nullptr);
@@ -924,15 +948,11 @@ int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8
       rc = run_moments(m);
     }
     if (rc) break;
-    if (contiguous_out && out_pitch == dopitch) {
-      CK(cudaMemcpyAsync(out + c0 * out_page_stride, dout, (size_t)(np * H * dopitch), cudaMemcpyDeviceToHost, s));
-    } else if (contiguous_out) {
-      CK(cudaMemcpy2DAsync(out + c0 * out_page_stride, out_pitch, dout, dopitch, orow, np * H,
-                           cudaMemcpyDeviceToHost, s));
+    if (contiguous_out) {
+      CK(copy_rows_d2h(out + c0 * out_page_stride, out_pitch, dout, dopitch, orow, np * H, s));
     } else {
       for (int64_t q = 0; q < np; ++q)
-        CK(cudaMemcpy2DAsync(out + (c0 + q) * out_page_stride, out_pitch, dout + q * dopage, dopitch, orow, H,
-                             cudaMemcpyDeviceToHost, s));
+        CK(copy_rows_d2h(out + (c0 + q) * out_page_stride, out_pitch, dout + q * dopage, dopitch, orow, H, s));
     }
   }
   for (int i = 0; i < nstr; ++i) {
@@ -1211,9 +1231,12 @@ int abin_stats(int32_t method, const uint8_t* in, int64_t H, int64_t W, int64_t 
 
 void abin_limits(abin_limits_t* out) {
   if (!out) return;
-  out->max_window_w = 190 * 8 - 1;
-  out->max_window_h = 66051;
+  out->max_window_w = 190 * 8 - 1;                // the CTA-wide kernel's halo (choose_nt_wide)
+  out->max_window_h = 66051;                      // 255^2 h < 2^32
+  out->max_window_hw = ((1ll << 32) - 1) / 255;   // 255 h w < 2^32
   out->max_dim = kMaxDim;
+  out->quantile_max_window_w = 3 * kQuantNT + 1;  // a thread stages at most 4 elements of a row
+  out->quantile_max_window_hw = 65535;            // u16 bins
 }
 
 const char* abin_strerror(int status) {
@@ -1228,7 +1251,7 @@ const char* abin_strerror(int status) {
   return "unknown status";
 }
 
-const char* abin_version(void) { return "abin 0.1 (sm_100a)"; }
+const char* abin_version(void) { return "abin 0.2 (sm_100a)"; }
 
 const char* abin_last_cuda_error(void) { return g_last_cuda_error; }
 

@@ -123,3 +123,40 @@ def test_product_path_does_not_touch_the_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, flags=re.M), f
                 assert "liboracle" not in txt and "abin_oracle" not in txt, f
+
+
+def test_limits_match_the_erange_checks(lib):
+    """abin_limits states what each path takes; one step beyond returns
+    ABIN_ERANGE before the device is touched (no compute call is made)."""
+    raw = lib.raw()
+    L = lib.limits()
+    assert L.max_dim == 1 << 30
+    assert L.max_window_hw == ((1 << 32) - 1) // 255
+    assert L.quantile_max_window_w == 385 and L.quantile_max_window_hw == 65535
+    H = W = 1000
+    q = lambda h, w: raw.abin_binarize_batched(3, FAKE_IN, H * W, FAKE_OUT, H * W, 1, H, W, W, W, 0, h, w, 0.5, 0.0,
+                                               -1, 0, None, None)
+    assert q(3, L.quantile_max_window_w + 1) == 3            # quantile width
+    assert q(256, 256) == 3                                  # h w > 65535
+    b = lambda h, w: raw.abin_binarize_batched(4, FAKE_IN, H * W, FAKE_OUT, H * W, 1, H, W, W, W, 0, h, w, -1.0, 0.0,
+                                               -1, 0, None, None)
+    assert b(3, L.quantile_max_window_w + 1) == 3            # Bernsen shares the histogram kernels
+    # moments: effective sizes are clamped to the image, so a huge window on a
+    # big (fake) image exceeds the width limit
+    big = 1 << 20
+    m = lambda h, w: raw.abin_binarize_batched(0, FAKE_IN, big, FAKE_OUT, big, 1, 8, big, big, big, 0, h, w, 0.5,
+                                               128.0, -1, 0, None, None)
+    assert m(3, L.max_window_w + 1) == 3
+
+
+def test_table1_rules_only_through_binarize_rule(lib):
+    # methods 5..8 need their parameter array: the batched / band / stats
+    # entry points reject them (ADVICE r1)
+    raw = lib.raw()
+    for method in (5, 6, 7, 8):
+        assert raw.abin_binarize_batched(method, FAKE_IN, 4096, FAKE_OUT, 4096, 1, 64, 64, 64, 64, 0, 5, 5, 0.5,
+                                         128.0, -1, 0, None, None) == 1
+        assert raw.abin_binarize_band(method, FAKE_IN, 50, 64, 64, 100, 400, 5, 5, FAKE_OUT, 64, 0, 11, 11, 0.5,
+                                      128.0, 7, 0, None, None) == 1
+        assert raw.abin_stats(method, FAKE_IN, 64, 64, 64, 5, 5, 0.5, 128.0, -1, None, None, None, None, None,
+                              None) == 1

@@ -519,3 +519,43 @@ def test_fixup_queue_and_overflow(monkeypatch, packed, cap, W):
         near += ref["near_tie"]
     assert near > 10_000
     assert int(cnt[0]) == near
+
+
+@pytest.mark.parametrize("packed", [False, True])
+@pytest.mark.parametrize("bands", [False, True])
+def test_host_io_touches_only_row_bytes(monkeypatch, packed, bands):
+    """ABIN_HOST_IO with 16-aligned padded pitches (the linear-copy case):
+    the input buffer ends right after the last row's W bytes, and the output
+    rows' padding bytes and the bytes after the last row are not written
+    (the copies once moved whole pitches)."""
+    if bands:
+        monkeypatch.setenv("ABIN_HOSTIO_CHUNK_BYTES", "20000")
+    P, H, W = 3, 120, 400
+    ip, op = 416, 432                                # 16-aligned pitches, padded
+    cols = (W + 7) // 8 if packed else W
+    pages = synth.pages(P, H, W, synth.config_seed(3, 77), stain=True)
+    in_len = (P * H - 1) * ip + W                    # nothing after the last row
+    out_len = (P * H - 1) * op + cols + 64           # 64 sentinel bytes after the last row
+    hin = torch.full((in_len,), 0xCD, dtype=torch.uint8).pin_memory()
+    hv = hin.numpy()
+    for p in range(P):
+        for i in range(H):
+            o = (p * H + i) * ip
+            hv[o:o + W] = pages[p, i]
+    hout = torch.full((out_len,), 0xAB, dtype=torch.uint8).pin_memory()
+    rc = abin.raw().abin_binarize_batched(
+        abin.SAUVOLA, abin.ctypes.c_void_p(hin.data_ptr()), H * ip, abin.ctypes.c_void_p(hout.data_ptr()), H * op, P,
+        H, W, ip, op, abin.MASK_BITS if packed else abin.MASK_U8, 31, 31, 0.5, 128.0, -1, abin.HOST_IO, None,
+        abin.ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    torch.cuda.synchronize()
+    ov = hout.numpy()
+    for p in range(P):
+        want = oracle.binarize("sauvola", pages[p], 31, 31, 0.5, 128.0)
+        want = oracle.pack_bits(want) if packed else want
+        for i in range(H):
+            o = (p * H + i) * op
+            assert np.array_equal(ov[o:o + cols], want[i]), (p, i)
+            pad_end = min(o + op, out_len)
+            assert (ov[o + cols:pad_end] == 0xAB).all(), (p, i)   # padding untouched
+    assert (ov[(P * H - 1) * op + cols:] == 0xAB).all()
