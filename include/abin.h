@@ -218,6 +218,23 @@ int abin_stats(int32_t method, const uint8_t* in, int64_t H, int64_t W, int64_t 
                double param0, double param1, int32_t L_override, uint64_t* c_out, uint64_t* d_out,
                uint32_t* n_out, double* t_out, uint8_t* mask_out, void* stream);
 
+/* ---- Test hook: the certified fp32 filter -----------
+ * Evaluates the production kernel's fp32 residual e~ = I - t~ (the device
+ * function residual_pair of moments5.cuh, shared with the kernel) for `count`
+ * tuples of exact window data: c = sum of I, d = sum of I^2 (c < 2^23,
+ * d < 2^32), ncol, nrow the window's column / row counts (n = ncol nrow,
+ * PAPER.md:118), I the centre pixel -- all device arrays of `count` entries;
+ * e_out (device, count floats) receives e~, s_out (optional) s~.  method is
+ * 0..2 (Sauvola, Niblack, Wolf with global minimum L).  bounds (optional,
+ * host, 5 doubles) receives the certified bound: [0] the coarse bound the
+ * kernel tests |e~| against, [1..4] rb0, rb1, rdv, rsdv of the data-dependent
+ * bound rb0 + rb1 min(rsdv, rdv / s~) (used for Niblack).  The claim the tests
+ * check: |e~ - e*| <= bound for the exact e* = I - t(c, d, n).  Asynchronous on
+ * `stream`; ABIN_EINVAL on bad arguments. */
+int abin_probe_filter(int32_t method, double k, double R, double L, const uint32_t* c, const uint32_t* d,
+                      const uint32_t* ncol, const uint32_t* nrow, const uint8_t* I, int64_t count, float* e_out,
+                      float* s_out, double* bounds, void* stream);
+
 /* ---- Limits, versions, errors ------------------------------------------------ */
 /* Effective windows are (min(l,W) + min(r,W)) x (min(o,H) + min(u,H))
  * (PAPER.md:94-97 clamped to the image: same in-bounds window, same n); a call

@@ -48,6 +48,7 @@ _lib.abin_binarize_band.argtypes = [_I32, _P, _I64, _I64, _I64, _I64, _I64, _I32
                                     _D, _D, _I32, _U32, _P, _P]
 _lib.abin_global_min.argtypes = [_P, _I64, _I64, _I64, _I64, _I64, _P, _P]
 _lib.abin_stats.argtypes = [_I32, _P, _I64, _I64, _I64, _I32, _I32, _D, _D, _I32, _P, _P, _P, _P, _P, _P]
+_lib.abin_probe_filter.argtypes = [_I32, _D, _D, _D, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P]
 _lib.abin_strerror.argtypes = [ctypes.c_int]
 _lib.abin_strerror.restype = ctypes.c_char_p
 _lib.abin_version.restype = ctypes.c_char_p
@@ -64,7 +65,7 @@ _lib.abin_limits.argtypes = [ctypes.POINTER(AbinLimits)]
 EXPORTED = ["abin_sauvola", "abin_niblack", "abin_wolf", "abin_quantile", "abin_bernsen", "abin_binarize_rule", "abin_otsu",
             "abin_binarize_batched",
             "abin_binarize_band", "abin_global_min", "abin_stats", "abin_limits", "abin_strerror", "abin_version",
-            "abin_last_cuda_error"]
+            "abin_last_cuda_error", "abin_probe_filter"]
 
 
 class AbinError(RuntimeError):
@@ -225,6 +226,20 @@ def global_min(pages: torch.Tensor, stream=None) -> torch.Tensor:
     L = torch.empty(P, dtype=torch.uint8, device=pages.device)
     _check(_lib.abin_global_min(_ptr(pages), pages.stride(0), P, H, W, pages.stride(1), _ptr(L), _stream(stream)))
     return L
+
+
+def probe_filter(method: str, c: torch.Tensor, d: torch.Tensor, ncol: torch.Tensor, nrow: torch.Tensor,
+                 I: torch.Tensor, k: float, R: float = 128.0, L: float = 0.0, stream=None):
+    """Test hook: the kernel's fp32 residuals e~ = I - t~ (and s~) for tuples
+    of exact window data (uint32 c, d, ncol, nrow; uint8 I, all on the device)
+    and the certified bound [coarse, rb0, rb1, rdv, rsdv] (abin.h)."""
+    n = c.numel()
+    e = torch.empty(n, dtype=torch.float32, device=c.device)
+    sv = torch.empty(n, dtype=torch.float32, device=c.device)
+    b = (ctypes.c_double * 5)()
+    _check(_lib.abin_probe_filter(METHODS[method], k, R, L, _ptr(c), _ptr(d), _ptr(ncol), _ptr(nrow), _ptr(I), n,
+                                  _ptr(e), _ptr(sv), b, _stream(stream)))
+    return e, sv, list(b)
 
 
 def stats(method: str, img: torch.Tensor, h: int, w: int, param0: float, param1: float = 128.0, L: int = -1,

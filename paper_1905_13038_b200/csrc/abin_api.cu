@@ -213,17 +213,15 @@ FilterConsts filter_consts(int method, double k, double R) {
 // expression.  Counts n lie in [n_min, n_max]; the start value and the
 // relative sums are window sums of windows with counts <= n_max, so they are
 // bounded by 255 n_max (c) and 255^2 n_max (d).
-FilterConsts filter_consts_v5(int method, double k, double R, double n_min, double n_max) {
+FilterConsts filter_consts_v5(int method, double k, double R) {
   const double u = std::ldexp(1.0, -24);
   const double eps_sqrt = 8 * u;            // sqrt.approx.f32: relative error < 2^-22 (taken as 2^-21)
   const double eps64 = 1e-6;                // |t_fp64 - t*| (the canonical double sequence)
-  const double e_nu = 3.01 * u;             // 1/ncol, 1/nrow and their product: three roundings
-  const double ratio = n_max / std::max(1.0, n_min);
+  const double e_nu = 3.01 * u;             // fl(fl(1/ncol) fl(1/nrow)): three roundings
   const double qmax = 255.0 * 255.0, smax = 127.5;
-  const double Mc = 255.0 * ratio;          // bound on |Sc| / n and |rel_c| / n
-  const double dm = 255.0 * (e_nu + 2.01 * u) + 1.01 * Mc * u;                  // |m~ - m|
-  const double dq = qmax * (e_nu + 1.01 * u) + 3.04 * qmax * ratio * u;        // |q~ - q|
-  const double dv = (2 * 255.0 + dm) * dm + dq + 1.01 * u * (smax * smax + 1.0);  // |(-w~) - v|
+  const double dm = 255.0 * (e_nu + u) * 1.01;                                // |m~ - m|: one rounding of c nu~
+  const double dq = qmax * (e_nu + 2 * u) * 1.01;                             // |q~ - q|: fl(d), then fl(fl(d) nu~)
+  const double dv = (2 * 255.0 + dm) * dm + dq + 1.01 * u * (smax * smax + 1.0);  // |(-w~) - v|, w~ = fl(m~^2 - q~)
   const double rv = std::sqrt(dv);
   const double ds = rv + eps_sqrt * (smax + rv);                               // |s~ - s| (coarse)
   FilterConsts f;
@@ -571,14 +569,7 @@ int run_moments(const MomCall& c) {
       if (use_v5) {
         q.KH = (win.w + kG - 1) / kG;
         q.Tw = kG * (32 - q.KH);
-        // counts n in [n_min, n_max] for this call: minima at the
-        // first/last column and at the call's first/last output row
-        auto ncol = [&](int64_t j) { return std::min<int64_t>(j + win.r, c.W - 1) - std::max<int64_t>(j - win.l, -1); };
-        auto nrow = [&](int64_t i) { return std::min<int64_t>(i + win.u, c.H_global - 1) - std::max<int64_t>(i - win.o, -1); };
-        const int64_t cmin = std::max<int64_t>(1, std::min(ncol(0), ncol(c.W - 1)));
-        const int64_t rmin = std::max<int64_t>(1, std::min(nrow(c.row0), nrow(c.row0 + c.H_out - 1)));
-        const FilterConsts f5 = filter_consts_v5(c.method, c.k, c.R, (double)(cmin * rmin),
-                                                 (double)win.h * (double)win.w);
+        const FilterConsts f5 = filter_consts_v5(c.method, c.k, c.R);
         q.fa = f5.fa; q.fb = f5.fb; q.delta1 = f5.delta1;
         q.rb0 = f5.rb0; q.rb1 = f5.rb1; q.rdv = f5.rdv; q.rsdv = f5.rsdv;
       }
@@ -1227,6 +1218,27 @@ int abin_stats(int32_t method, const uint8_t* in, int64_t H, int64_t W, int64_t 
   cudaError_t f = cudaFreeAsync(scratch, st);
   if (rc == ABIN_OK && f != cudaSuccess) return cuda_fail(f);
   return rc;
+}
+
+int abin_probe_filter(int32_t method, double k, double R, double L, const uint32_t* c, const uint32_t* d,
+                      const uint32_t* ncol, const uint32_t* nrow, const uint8_t* I, int64_t count, float* e_out,
+                      float* s_out, double* bounds, void* stream) {
+  if (method < ABIN_SAUVOLA || method > ABIN_WOLF || count < 0) return ABIN_EINVAL;
+  if (!std::isfinite(k) || !std::isfinite(R) || !(R > 0.0) || !std::isfinite(L)) return ABIN_EINVAL;
+  const FilterConsts f = filter_consts_v5(method, k, R);
+  if (bounds) {
+    bounds[0] = f.delta1; bounds[1] = f.rb0; bounds[2] = f.rb1; bounds[3] = f.rdv; bounds[4] = f.rsdv;
+  }
+  if (count == 0) return ABIN_OK;
+  if (!c || !d || !ncol || !nrow || !I || !e_out) return ABIN_EINVAL;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned nb = (unsigned)((count + 255) / 256);
+  const float Lf = (float)L;
+  if (method == M_SAUVOLA) v5::k_probe<M_SAUVOLA><<<nb, 256, 0, st>>>(c, d, ncol, nrow, I, count, f.fa, f.fb, Lf, e_out, s_out);
+  else if (method == M_NIBLACK) v5::k_probe<M_NIBLACK><<<nb, 256, 0, st>>>(c, d, ncol, nrow, I, count, f.fa, f.fb, Lf, e_out, s_out);
+  else v5::k_probe<M_WOLF><<<nb, 256, 0, st>>>(c, d, ncol, nrow, I, count, f.fa, f.fb, Lf, e_out, s_out);
+  CK(cudaGetLastError());
+  return ABIN_OK;
 }
 
 void abin_limits(abin_limits_t* out) {

@@ -163,6 +163,39 @@ __device__ __forceinline__ void method_consts(float fa, float fb, f2& fa2, f2& f
   else { fa2 = splat(-fa); fb2 = splat(-fb); }
 }
 
+// The certified residual pair from the exact window sums (the epilogue of
+// the kernel and of the filter probe, abin_probe_filter):
+//   cb = bits of the float 2^23 + c (c < 2^23), d the window square sum,
+//   nu = -1/n as fl(fl(1/ncol) fl(1/nrow)), nb = -2^23 nu (exact), I exact.
+// -m~ = fl((2^23 + c) nu + nb): the product is exact inside the fma, so this
+// is the correctly rounded c (-1/n); -q~ = fl(fl(d) nu).
+template <int METHOD>
+__device__ __forceinline__ f2 residual_pair(uint32_t cb0, uint32_t cb1, uint32_t d0, uint32_t d1, f2 nu, f2 nb, f2 I,
+                                            f2 fa2, f2 fb2, f2 Lf2, f2& s) {
+  const f2 mn = fma2(pk(__uint_as_float(cb0), __uint_as_float(cb1)), nu, nb);
+  const f2 qn = mul2(pk((float)d0, (float)d1), nu);
+  return residual2<METHOD>(mn, qn, I, fa2, fb2, Lf2, s);
+}
+
+// The filter probe: one tuple (c, d, ncol, nrow, I) per thread, evaluated by
+// residual_pair exactly as the kernel does (a test hook for the certified
+// bound; the host checks |e~ - e*| <= the bound over many tuples).
+template <int METHOD>
+__global__ void k_probe(const uint32_t* c, const uint32_t* d, const uint32_t* ncol, const uint32_t* nrow,
+                        const uint8_t* I, int64_t count, float fa, float fb, float Lf, float* e_out, float* s_out) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const float nu1 = -(__frcp_rn((float)ncol[q]) * __frcp_rn((float)nrow[q]));
+  const f2 nu = splat(nu1), nb = mul2(nu, splat(-8388608.0f));
+  f2 fa2, fb2;
+  method_consts<METHOD>(fa, fb, fa2, fb2);
+  const float If = (float)I[q];
+  f2 sv;
+  const f2 e = residual_pair<METHOD>(kBias + c[q], kBias + c[q], d[q], d[q], nu, nb, pk(If, If), fa2, fb2, splat(Lf), sv);
+  e_out[q] = lo(e);
+  if (s_out) s_out[q] = lo(sv);
+}
+
 // Kernel template parameters:
 //   W32   w mod 32: fixes the byte offset DL = r mod 16 of the lane's columns
 //         in the staged rows and the phase RHO = (-w) mod 16 of its leaving
@@ -463,16 +496,12 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
             nu = mul2(pk(nc.x, nc.y), splat(inv_nrow));
             nb = mul2(nu, splat(-8388608.0f));
           }
-          // -m~ = fl((2^23 + c)(-1/n) - 2^23 (-1/n)): the product is exact inside
-          // the fma, so this is the correctly rounded c (-1/n)
-          const f2 mn = fma2(pk(__uint_as_float(cq[0]), __uint_as_float(cq[1])), nu, nb);
-          const f2 qn = mul2(pk((float)dq[0], (float)dq[1]), nu);                                    // -q~
           // I exactly: the byte as 32768 + I, minus 32768
           const f2 I = add2(pk(__uint_as_float(__byte_perm(wd, kMagic, 0x7504u | ((uint32_t)h2 << 4))),
                                __uint_as_float(__byte_perm(wd, kMagic, 0x7504u | ((uint32_t)(h2 + 1) << 4)))),
                             M32);
           f2 sv;
-          const f2 e = residual2<METHOD>(mn, qn, I, fa2, fb2, Lf2, sv);
+          const f2 e = residual_pair<METHOD>(cq[0], cq[1], dq[0], dq[1], nu, nb, I, fa2, fb2, Lf2, sv);
           emin = fmin3(emin, fabsf(lo(e)), fabsf(hi(e)));
           if (METHOD == M_NIBLACK) smin = fmin3(smin, lo(sv), hi(sv));
           e4[h2] = lo(e);

@@ -1,0 +1,132 @@
+"""The certified fp32 filter's error bound, checked directly (-m gpu).
+
+The v5 kernel decides a pixel in fp32 when its residual e~ = I - t~ is
+farther from 0 than a host-derived bound, and queues it for the exact stages
+otherwise.  Masks equal the fp64 decision only if the
+bound holds: |e~ - e*| <= bound, e* = I - t(c, d, n) exactly.  Here the
+production arithmetic (abin_probe_filter runs the kernel's own device
+function on given tuples) is compared with e* evaluated on the host from the
+exact integers (V = n d - c^2 in int64, then 80-bit long double), on 1.08e8
+random realizable tuples (n = ncol nrow within the v5 domain, c in [0, 255 n],
+d in [c^2/n, 255 c], I in [0, 255]) plus adversarial ones: near ties
+(I = round(t*)), minimum-variance and constant windows, maximum-variance
+windows, the smallest and largest counts.  SURVEY section 8(c) test (ii).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1905_13038_b200 import abin  # noqa: E402
+
+DEV = torch.device("cuda:0")
+LD = np.longdouble
+CHUNK = 4_000_000
+CHUNKS = 9                     # x 3 methods = 1.08e8 random tuples
+PARAMS = {"sauvola": (0.5, 128.0, 0.0), "niblack": (-0.2, 128.0, 0.0), "wolf": (0.5, 128.0, 17.0)}
+
+
+def t_exact(method, c, d, n, k, R, L):
+    V = n.astype(np.int64) * d.astype(np.int64) - c.astype(np.int64) ** 2   # exact (< 2^63)
+    assert (V >= 0).all()
+    nl = n.astype(LD)
+    m = c.astype(LD) / nl
+    s = np.sqrt(V.astype(LD) / (nl * nl))
+    k, R, L = LD(k), LD(R), LD(L)
+    if method == "sauvola":
+        return m * (1 + k * (s / R - 1))
+    if method == "niblack":
+        return m + k * s
+    return m - k * (m - L) * (1 - s / R)
+
+
+def random_tuples(rng, count):
+    ncol = rng.integers(1, 128, count, dtype=np.int64)
+    nrow = rng.integers(1, 130, count, dtype=np.int64)
+    big = rng.random(count) < 0.5                      # half at the configs' interior sizes
+    ncol[big] = rng.choice([15, 31, 32, 61, 63, 101, 127], int(big.sum()))
+    nrow[big] = ncol[big]
+    nrow = np.minimum(nrow, 129)
+    n = ncol * nrow
+    c = (rng.random(count) * (255 * n + 1)).astype(np.int64)
+    lo = -(-(c * c) // n)                              # ceil(c^2 / n)
+    hi = np.minimum(255 * c, 255 * 255 * n)
+    d = lo + (rng.random(count) * (hi - lo + 1)).astype(np.int64)
+    d = np.minimum(d, hi)
+    I = rng.integers(0, 256, count, dtype=np.int64)
+    return c, d, ncol, nrow, I
+
+
+def adversarial_tuples(rng, method, count):
+    k, R, L = PARAMS[method]
+    c, d, ncol, nrow, I = random_tuples(rng, count)
+    n = ncol * nrow
+    q = count // 6
+    # minimum variance (d = ceil(c^2/n)) and constant windows (c = n g, d = n g^2)
+    d[:q] = -(-(c[:q] * c[:q]) // n[:q])
+    g = rng.integers(0, 256, q)
+    c[q:2 * q], d[q:2 * q] = n[q:2 * q] * g, n[q:2 * q] * g * g
+    # maximum variance: half 0, half 255
+    nn = n[2 * q:3 * q]
+    c[2 * q:3 * q] = 255 * (nn // 2)
+    d[2 * q:3 * q] = 255 * 255 * (nn // 2)
+    # extreme counts
+    ncol[3 * q:3 * q + q // 2], nrow[3 * q:3 * q + q // 2] = 1, 1
+    ncol[3 * q + q // 2:4 * q], nrow[3 * q + q // 2:4 * q] = 127, 129
+    n = ncol * nrow
+    c = np.minimum(c, 255 * n)
+    lo = -(-(c * c) // n)
+    d = np.clip(d, lo, np.minimum(255 * c, 255 * 255 * n))
+    # near ties everywhere: I = round(t*)
+    t = t_exact(method, c, d, n, k, R, L)
+    I = np.clip(np.rint(t.astype(np.float64)), 0, 255).astype(np.int64)
+    return c, d, ncol, nrow, I
+
+
+def run_probe(method, c, d, ncol, nrow, I):
+    k, R, L = PARAMS[method]
+    dev = lambda a, dt: torch.from_numpy(a.astype(dt)).to(DEV)
+    e, sv, b = abin.probe_filter(method, dev(c, np.uint32), dev(d, np.uint32), dev(ncol, np.uint32),
+                                 dev(nrow, np.uint32), dev(I, np.uint8), k, R, L)
+    return e.cpu().numpy().astype(LD), sv.cpu().numpy().astype(np.float64), b
+
+
+def check(method, c, d, ncol, nrow, I):
+    k, R, L = PARAMS[method]
+    e, sv, b = run_probe(method, c, d, ncol, nrow, I)
+    e_star = I.astype(LD) - t_exact(method, c, d, ncol * nrow, k, R, L)
+    err = np.abs(e - e_star).astype(np.float64)
+    coarse = b[0]
+    assert err.max() <= coarse, (method, err.max(), coarse)
+    ratio = err.max() / coarse
+    if method == "niblack":
+        # the data-dependent bound the kernel applies to Niblack lanes
+        with np.errstate(divide="ignore"):
+            refined = b[1] + b[2] * np.minimum(b[4], b[3] / sv)
+        assert (err <= refined).all(), (method, (err - refined).max())
+        ratio = max(ratio, (err / refined).max())
+    return ratio
+
+
+@pytest.mark.parametrize("method", ["sauvola", "niblack", "wolf"])
+def test_certified_bound_random(method):
+    rng = np.random.default_rng({"sauvola": 1, "niblack": 2, "wolf": 3}[method])
+    worst = 0.0
+    for _ in range(CHUNKS):
+        worst = max(worst, check(method, *random_tuples(rng, CHUNK)))
+    assert worst < 1.0
+    print(f"{method}: {CHUNKS * CHUNK} random tuples, max |e~ - e*| / bound = {worst:.3g}")
+
+
+@pytest.mark.parametrize("method", ["sauvola", "niblack", "wolf"])
+def test_certified_bound_adversarial(method):
+    rng = np.random.default_rng({"sauvola": 11, "niblack": 12, "wolf": 13}[method])
+    worst = 0.0
+    for _ in range(3):
+        worst = max(worst, check(method, *adversarial_tuples(rng, method, 1_000_000)))
+    assert worst < 1.0
+    print(f"{method}: 3e6 adversarial tuples, max |e~ - e*| / bound = {worst:.3g}")
