@@ -1,14 +1,21 @@
 """bench.py -- the driver's benchmark contract for the abin hot path.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 3]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 1|2|3|4|5|5b] [--scaling strong|weak]
 
 One step = one pass of the whole hot path (moments -> Sauvola threshold ->
 mask) over one batch of synthetic pages resident in HBM.  The default
 workload is BASELINE.json config 3 (the large-page config the >= 70 % roofline
-target is quoted on): 64 pages of 7016 x 4960 uint8 (A4 @ 600 dpi) with the
-stain blob, Sauvola k = 0.5, R = 128, h = w = 61, byte mask.  Pages are
-independent, so N GPUs each binarize their own 64-page batch (weak scaling,
-no data-path collective).  Rank 0 prints one JSON line.
+target is quoted on): a batch of 64 pages of 7016 x 4960 uint8 (A4 @ 600 dpi)
+with the stain blob, Sauvola k = 0.5, R = 128, h = w = 61, byte mask.  Pages
+are independent: at N GPUs the 64-page batch is sharded 64/N pages per rank
+(strong scaling, BASELINE configs[2]; no data-path collective); --scaling weak
+gives every rank its own 64 pages instead.  --config 5b is BASELINE configs[4]'s
+page batch: 32 pages of 4096^2, local median 51x51, sharded over the ranks.
+--config 2 times the window sweep h = w in {15, 31, 63, 127, 255} (one step =
+the five windows) and reports each window and the flatness (max / median).
+--config 4 at N > 1 splits the 32768^2 scan into row bands with NCCL halos.
+Rank 0 prints one JSON line.
 
 --impl reference times the CPU oracle (oracle/, the only other place bench.py
 executes it) on the host cores, on a bounded sample of the same workload.
@@ -43,7 +50,14 @@ CONFIGS = {
         "config4: 1 page 32768x32768 u8, Sauvola k=0.34 R=128 h=w=101, forced u64 square sums, bit mask"),
     5: (1, 4096, 4096, 51, 51, "quantile", 0.5, 0.0, False, False,
         "config5: 1 page 4096x4096 u8, local median (q=0.5) 51x51, u8 mask"),
+    "5b": (32, 4096, 4096, 51, 51, "quantile", 0.5, 0.0, False, False,
+           "config5b: batch of 32 pages 4096x4096 u8, local median (q=0.5) 51x51, u8 mask"),
 }
+SWEEP = (15, 31, 63, 127, 255)  # config 2's windows (BASELINE configs[1])
+
+
+def cfg_key(c):
+    return c if c == "5b" else int(c)
 
 
 def measured_peaks():
@@ -144,16 +158,33 @@ def dist_env():
     return world, rank, local
 
 
+def page_shard(P, rank, world, scaling):
+    """(first page, pages) of this rank: the batch sharded contiguously and
+    balanced (strong scaling), or a whole batch per rank (weak)."""
+    if scaling == "weak" or world == 1:
+        return rank * P, P
+    base, extra = divmod(P, world)
+    return rank * base + min(rank, extra), base + (1 if rank < extra else 0)
+
+
 def make_pages(cfg, rank, scaling, world):
     P, H, W, h, w, method, k, R, packed, stain, _ = CONFIGS[cfg]
-    if scaling == "strong" and P > 1:
-        P = (P + world - 1) // world
-        first = rank * P
-    else:
-        first = rank * P
-    pages = np.empty((P, H, W), np.uint8)
-    synth.pages(P, H, W, synth.config_seed(cfg, first), stain=stain, out=pages)
+    first, n = page_shard(P, rank, world, scaling)
+    pages = np.empty((n, H, W), np.uint8)
+    seed_cfg = 5 if cfg == "5b" else cfg
+    if n:
+        synth.pages(n, H, W, synth.config_seed(seed_cfg, first), stain=stain, out=pages)
     return pages
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def reference_main(args):
@@ -165,7 +196,7 @@ def reference_main(args):
     cfg = args.config
     P, H, W, h, w, method, k, R, packed, stain, label = CONFIGS[cfg]
     page = np.empty((H, W), np.uint8)
-    synth.page(H, W, synth.config_seed(cfg, 0), stain=stain, out=page)
+    synth.page(H, W, synth.config_seed(5 if cfg == "5b" else cfg, 0), stain=stain, out=page)
     cores = oracle.num_threads()
     # bounded sample: a full-width band of rows of page 0, sized (from a
     # calibration band) so the whole warm-up + timed run takes ~2 minutes
@@ -188,9 +219,11 @@ def reference_main(args):
     sample = f"rows 0..{rows - 1} (full width {W}) of page 0 of {label}; {px} px per step"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tmean * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic",
+            "scaling": "strong" if cfg in (3, "5b", 4) and args.scaling == "strong" else "weak",
+            "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic",
             "config": {"workload": label, "sample_rows": rows},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(),
+                             "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -212,7 +245,7 @@ def cpu_baseline(cfg, budget_s=12.0):
     import oracle
     P, H, W, h, w, method, k, R, packed, stain, label = CONFIGS[cfg]
     page = np.empty((H, W), np.uint8)
-    synth.page(H, W, synth.config_seed(cfg, 0), stain=stain, out=page)
+    synth.page(H, W, synth.config_seed(5 if cfg == "5b" else cfg, 0), stain=stain, out=page)
     rows = min(H, 4)
     t0 = time.perf_counter()
     _oracle_band(oracle, method, page, rows, h, w, k, R)
@@ -222,7 +255,8 @@ def cpu_baseline(cfg, budget_s=12.0):
     _oracle_band(oracle, method, page, rows2, h, w, k, R)
     dt2 = time.perf_counter() - t0
     px = rows2 * W
-    return {"value": px / dt2 / 1e9, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+    return {"value": px / dt2 / 1e9, "unit": UNIT, "cores": oracle.num_threads(), "cpu_model": cpu_model(),
+            "kind": "oracle",
             "sample": f"direct definition on rows 0..{rows2 - 1} (full width) of page 0 of {label}: "
                       f"{px} px in {dt2:.2f} s"}
 
@@ -257,6 +291,10 @@ def ours_main(args):
 
     cfg = args.config
     P0, H, W, h, w, method, k, R, packed, stain, label = CONFIGS[cfg]
+    sweep = cfg == 2
+    if sweep:
+        label = ("config2: 1 page 3300x2550 u8 (letter @300dpi), Sauvola k=0.5 R=128, window sweep h=w in "
+                 + "{" + ",".join(map(str, SWEEP)) + "} (one step = the five windows), u8 mask")
     cols = (W + 7) // 8 if packed else W
     flags = abin.FORCE_U64_SQ if cfg == 4 else 0
     counters = torch.zeros(2, dtype=torch.int64, device=dev)
@@ -287,7 +325,7 @@ def ours_main(args):
     else:
         pages_np = make_pages(cfg, rank, args.scaling, world)
         P = pages_np.shape[0]
-        step_bytes = P * H * W * (1 + cols / W)
+        step_bytes = max(1, P) * H * W * (1 + cols / W)
         # inputs larger than L2: rotate through enough copies that a step never
         # finds its page (or its mask) in the 126 MB L2
         n_copies = 1 if step_bytes > 4 * L2_BYTES else int(min(2048, -(-3 * L2_BYTES // step_bytes)))
@@ -298,19 +336,31 @@ def ours_main(args):
         out = outs[0]
         px_rank = P * H * W
 
+        sweep_ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                     for _ in SWEEP] for _ in range(args.steps + args.warmup)] if sweep else None
+
         def step(i):
+            if P == 0:
+                return
             x, o = xs[i % n_copies], outs[i % n_copies]
-            if P == 1:
+            if sweep:
+                for z, hw in enumerate(SWEEP):
+                    sweep_ev[i][z][0].record(stream)
+                    ab.sauvola(x[0], hw, hw, k, R, packed=packed, out=o[0], flags=flags, counters=counters)
+                    sweep_ev[i][z][1].record(stream)
+            elif P == 1:
                 if method == "quantile":
                     ab.quantile(x[0], h, w, k, packed=packed, out=o[0])
                 else:
                     ab.sauvola(x[0], h, w, k, R, packed=packed, out=o[0], flags=flags, counters=counters)
             else:
                 ab.binarize_batched(method, x, h, w, k, R, packed=packed, out=o, flags=flags, counters=counters)
-        # quantile: one kernel; moments: v4 + exact fixup + v3 overflow
-        # follow-up (its CTAs exit at once unless the fixup queue overflowed);
-        # Wolf adds the fill + global-minimum pre-pass
-        launches_per_step = 1 if method == "quantile" else (5 if method == "wolf" else 3)
+        # quantile: one kernel; moments: the v5 kernel + exact fixup (+ the v3
+        # overflow follow-up when the queue could overflow: its CTAs exit at
+        # once unless it did); Wolf adds the fill + global-minimum pre-pass
+        launches_per_step = 0 if P == 0 else (1 if method == "quantile" else (5 if method == "wolf" else 3))
+        if sweep:
+            launches_per_step = 3 * len(SWEEP)
         l2_note = (f"inputs {step_bytes / 1e9:.2f} GB per rank per step > L2: no flush needed" if n_copies == 1 else
                    f"L2-resident workload: steps rotate through {n_copies} input/mask copies "
                    f"({n_copies * step_bytes / 1e6:.0f} MB > 126 MB L2), no step reuses a cached page")
@@ -344,14 +394,26 @@ def ours_main(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
 
-    px_total = px_rank * world
+    px_step = px_rank * (len(SWEEP) if sweep else 1)
+    pt = torch.tensor([float(px_step)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(pt, op=dist.ReduceOp.SUM)
+    px_total = float(pt.item())          # pixels of all ranks per step
     value = px_total * args.steps / (max_ms / 1e3) / 1e9
     ms_per_step = max_ms / args.steps
+    sweep_rows = None
+    if sweep:
+        sweep_rows = []
+        for z, hw in enumerate(SWEEP):
+            ms = [sweep_ev[args.warmup + i][z][0].elapsed_time(sweep_ev[args.warmup + i][z][1])
+                  for i in range(args.steps)]
+            msz = statistics.median(ms)
+            sweep_rows.append({"h": hw, "w": hw, "ms": msz, "gpx_s": px_rank / msz / 1e6})
 
     # --- roofline of the dominant kernel: algorithmic bytes / launch time
     bytes_per_px = 1.0 + (0.125 if packed else 1.0)
     avg_kern_s = (sum(kern_ms) / len(kern_ms)) / 1e3
-    achieved = px_rank * bytes_per_px / avg_kern_s / 1e9
+    achieved = px_step * bytes_per_px / avg_kern_s / 1e9
     peak, peak_kind = measured_peaks()
     traffic = None if banded else ncu_traffic(cfg, px_rank)
 
@@ -371,14 +433,15 @@ def ours_main(args):
                 hout.copy_(out, non_blocking=True)
             h2d, d2h = host_own.numel(), hout.numel()
         else:
-            # a bounded slice of the batch keeps the pinned host memory per rank
-            # small (eight ranks of 64 pages would pin ~36 GB); the metric is a
-            # rate, the per-page cost is the same
-            Pe = min(P, 16)
+            # the rank's whole shard (the headline batch: 64 pages at N = 1, 64/N
+            # per rank under strong scaling), pinned; capped at 64 pages
+            Pe = min(P, 64)
             hin = torch.from_numpy(np.ascontiguousarray(pages_np[:Pe])).pin_memory()
             hout = torch.empty((Pe, H, cols), dtype=torch.uint8).pin_memory()
 
             def e2e_step():
+                if Pe == 0:
+                    return
                 # abin_binarize_batched with ABIN_HOST_IO: the library streams
                 # the pages through device staging, copies overlapped with compute
                 rc = abin.raw().abin_binarize_batched(
@@ -405,7 +468,10 @@ def ours_main(args):
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e_ms = float(et.item()) / e2e_steps
-        e2e_px = (hout.shape[0] * H * W if not banded else px_rank) * world
+        pe = torch.tensor([float(hout.shape[0] * H * W if not banded else px_rank)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(pe, op=dist.ReduceOp.SUM)
+        e2e_px = float(pe.item())
         ok = torch.equal(hout, out.cpu() if banded else out[:hout.shape[0]].cpu())
         e2e = {"value": e2e_px / (e2e_ms / 1e3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms, "steps": e2e_steps,
@@ -415,15 +481,26 @@ def ours_main(args):
     if rank == 0:
         cfgd = {"workload": label, "H": H, "W": W, "h": h, "w": w, "method": method, "k": k, "R": R,
                 "mask": "bits" if packed else "u8", "l2": l2_note}
+        if sweep:
+            med = statistics.median(r["gpx_s"] for r in sweep_rows)
+            cfgd.update(h="sweep", w="sweep", window_sweep=sweep_rows,
+                        flatness={"max_over_median": max(r["gpx_s"] for r in sweep_rows) / med,
+                                  "min_over_median": min(r["gpx_s"] for r in sweep_rows) / med,
+                                  "criterion": "within +-20% of the median (SPEC.md:457)"})
         if banded:
             cfgd.update(decomposition=f"{world} row bands, halo {h // 2} rows below / {(h + 1) // 2 - 1} above "
                                       "via NCCL send/recv", rows_per_rank=px_rank // W)
         else:
-            cfgd.update(pages_per_rank=P, decomposition="pages sharded by rank (no data-path collective)")
+            strong = args.scaling == "strong" and P0 > 1
+            cfgd.update(pages_per_rank=P, batch_pages=P0 if strong else P0 * world,
+                        decomposition=(f"batch of {P0} pages sharded {P0}/{world} per rank" if strong else
+                                       ("every rank its own batch" if P0 > 1 else "one page per rank (replicas)"))
+                        + " (no data-path collective)")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak" if not banded else "strong", "vs_baseline": None, "dtype": "u32/f64",
+            "scaling": "strong" if banded or (args.scaling == "strong" and P0 > 1) else "weak",
+            "vs_baseline": None, "dtype": "u32/f64",
             "data": "synthetic", "config": cfgd,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -451,8 +528,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--config", type=cfg_key, default=3, choices=list(CONFIGS))
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -167,7 +167,14 @@ def run_band(method: str, band: Band, h: int, w: int, param0: float, param1: flo
         out = torch.empty((n, cols), dtype=torch.uint8, device=band.buf.device)
     if method == "wolf" and L < 0:
         raise ValueError("Wolf on bands needs the whole image's minimum: pass L (see global_min_bands)")
+    # NVTX ranges (an nsys trace shows the halo exchange overlapping the
+    # interior rows); no-ops without a profiler and on CPU tensors
+    nvtx = torch.cuda.nvtx if band.buf.is_cuda else None
+    if nvtx:
+        nvtx.range_push("abin.halo_exchange_post")
     works = exchange_halos(band, rank, world, h, group) if exchange else []
+    if nvtx:
+        nvtx.range_pop()
     kw = dict(param0=param0, param1=param1, L=L, packed=packed, flags=flags, counters=counters)
     # rows whose windows need the top / bottom halo
     a = min(o - 1, r0)                       # = band.top
@@ -175,8 +182,14 @@ def run_band(method: str, band: Band, h: int, w: int, param0: float, param1: flo
     lo, hi = min(a, n), max(min(a, n), n - b)
     own0 = band.top                          # buffer row of global row r0
     if hi > lo:                              # interior: held rows = own rows only
+        if nvtx:
+            nvtx.range_push("abin.band_interior")
         held = band.buf[own0:own0 + n]
         binarize_band(method, held, r0 + lo, H, lo, n - hi, h, w, out=out[lo:hi], **kw)
+        if nvtx:
+            nvtx.range_pop()
+    if nvtx:
+        nvtx.range_push("abin.halo_wait_and_edges")
     for wk in works:
         wk.wait()
     if lo > 0:                               # top strip: rows [r0, r0 + lo)
@@ -187,6 +200,8 @@ def run_band(method: str, band: Band, h: int, w: int, param0: float, param1: flo
         first = own0 + hi - min(o - 1, r0 + hi)
         held = band.buf[first:own0 + n + band.bot]
         binarize_band(method, held, r0 + hi, H, min(o - 1, r0 + hi), band.bot, h, w, out=out[hi:], **kw)
+    if nvtx:
+        nvtx.range_pop()
     return out
 
 
