@@ -56,6 +56,10 @@ def _load():
         lib.orc_binarize.argtypes = [_I32, _P, _I64, _I64, _I64, _I32, _I32, _D, _D, _I32, _P, _P, _P, _P, _P, _P]
         lib.orc_binarize_points.argtypes = [_I32, _P, _I64, _I64, _I64, _I32, _I32, _D, _D, _I32, _I64, _P, _P,
                                             _P, _P, _P, _P, _P]
+        lib.orc_max_s.argtypes = [_P, _I64, _I64, _I64, _I32, _I32]
+        lib.orc_max_s.restype = _D
+        lib.orc_adaptive_R.argtypes = [_D]
+        lib.orc_adaptive_R.restype = _D
         lib.orc_alg1_stats.argtypes = [_P, _I64, _I64, _I64, _I32, _I32, _P, _P]
         lib.orc_integral_stats.argtypes = [_P, _I64, _I64, _I64, _I32, _I32, _P, _P]
         lib.orc_quantile.argtypes = [_P, _I64, _I64, _I64, _I32, _I32, _D, _P, _P]
@@ -108,6 +112,17 @@ def count(H, W, h, w, i, j) -> int:
 def threshold(method: str, c: int, d: int, n: int, k: float, R: float = 128.0, L: float = 0.0) -> float:
     """Canonical fp64 threshold from exact (c, d, n) -- Table 1, left to right."""
     return float(_load().orc_threshold(_METHODS[method], c, d, n, k, R, L))
+
+
+def max_s(I, h: int, w: int) -> float:
+    """Wolf's adaptive R source: max over the page of the canonical fp64 s."""
+    I = _img(I)
+    return _load().orc_max_s(I.ctypes.data, I.shape[0], I.shape[1], I.strides[0], h, w)
+
+
+def adaptive_R(I, h: int, w: int) -> float:
+    """R = max s, or +inf when every window is constant (R21)."""
+    return _load().orc_adaptive_R(max_s(I, h, w))
 
 
 def global_min(I) -> int:

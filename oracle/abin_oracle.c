@@ -125,6 +125,34 @@ double orc_threshold(int32_t method, uint64_t c, uint64_t d, uint64_t n, double 
   return NAN;
 }
 
+/* Wolf's image-adaptive dynamic range R (NEXT #3; PAPER.md:153 writes Wolf's
+ * rule with a constant R; Wolf et al.'s original takes R = the maximum of s
+ * over the image -- SPEC.md:303, 319, "two-pass mode"; reading R21):
+ * the maximum over the page's pixels of s, each s by the canonical fp64
+ * sequence of orc_threshold (m = c/n, v = d/n - m m clamped at 0, s = sqrt v).
+ * A page whose windows are all constant has max s = 0: R is then +inf, so
+ * s / R = 0 and Wolf's t = m - k (m - L) (the reading R21). */
+double orc_max_s(const uint8_t *I, int64_t H, int64_t W, int64_t pitch, int32_t h, int32_t w) {
+  double best = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : best)
+  for (int64_t i = 0; i < H; ++i) {
+    for (int64_t j = 0; j < W; ++j) {
+      uint64_t c, d;
+      direct_sums(I, H, W, pitch, h, w, i, j, &c, &d);
+      const uint64_t n = (uint64_t)orc_count(H, W, h, w, i, j);
+      double m = (double)c / (double)n;
+      double v = (double)d / (double)n - m * m;
+      if (v < 0) v = 0;
+      const double sv = sqrt(v);
+      if (sv > best) best = sv;
+    }
+  }
+  return best;
+}
+
+/* R for Wolf's adaptive mode from the maximum s (R21). */
+double orc_adaptive_R(double max_s) { return max_s > 0.0 ? max_s : INFINITY; }
+
 /* Global minimum of gray levels, Table 1 notation L. */
 int32_t orc_global_min(const uint8_t *I, int64_t H, int64_t W, int64_t pitch) {
   int32_t L = 255;

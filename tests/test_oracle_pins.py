@@ -650,3 +650,47 @@ def test_feng_exact_with_gamma():
         pw = lambda e: Decimal(0) if x == 0 else (e * x.ln()).exp()
         exact = A1 * m + K1 * pw(1 + G) * (m - L) + K2 * pw(G) * L
         assert _close(tq, exact, 1e-10), (i, j, tq, exact)
+
+
+# ------------------------------- Wolf with image-adaptive R (NEXT #3, R21)
+
+def _exact_s_all(I, h, w):
+    """Every pixel's exact s (Decimal, from the window's pixel list)."""
+    H, W = I.shape
+    return [[_dec_window(I, h, w, i, j)[1] for j in range(W)] for i in range(H)]
+
+
+def test_max_s_brute_force():
+    # the oracle's fp64 max s equals the exact maximum of s over the page to
+    # within the fp64 sequence's rounding, on pages small enough to enumerate
+    for seed, (H, W, h, w) in enumerate([(9, 11, 3, 5), (12, 7, 4, 4), (10, 13, 7, 3), (6, 6, 11, 11)]):
+        I = synth.page(H, W, synth.config_seed(9, 60 + seed), stain=True)
+        exact = max(max(row) for row in _exact_s_all(I, h, w))
+        got = oracle.max_s(I, h, w)
+        assert abs(Decimal(got) - exact) <= Decimal("1e-12") * max(Decimal(1), exact), (seed, got, exact)
+        # teeth: the maximum of m or of v would be far off
+        assert abs(Decimal(got) ** 2 - exact ** 2) < Decimal("1e-9") * max(Decimal(1), exact ** 2)
+
+
+def test_max_s_closed_forms_and_adaptive_R():
+    # constant page: every window is constant, max s = 0, R = +inf (R21):
+    # Wolf's t = m - k (m - L) = g, an exact tie, so the page is foreground
+    g = synth.constant(15, 17, 90)
+    assert oracle.max_s(g, 5, 5) == 0.0 and oracle.adaptive_R(g, 5, 5) == float("inf")
+    assert (oracle.binarize("wolf", g, 5, 5, 0.5, float("inf")) == 0).all()
+    # a window covering the whole page: every s is the page's standard deviation
+    I = synth.uniform_random(11, 14, 61)
+    assert abs(oracle.max_s(I, 2 * 11 + 1, 2 * 14 + 1) - I.std()) < 1e-9
+    # half 0 / half 255 inside one window: s = 127.5, the largest possible
+    J = np.zeros((8, 8), np.uint8)
+    J[:, 4:] = 255
+    assert oracle.max_s(J, 8, 8) == 127.5
+    # transposition invariance (h <-> w)
+    K = synth.page(13, 19, synth.config_seed(9, 70), stain=True)
+    assert oracle.max_s(K, 5, 7) == oracle.max_s(np.ascontiguousarray(K.T), 7, 5)
+    # adaptive R >= every pixel's s, so Wolf's (1 - s/R) >= 0: t lies in [L, m]
+    R = oracle.adaptive_R(K, 5, 7)
+    st = oracle.binarize("wolf", K, 5, 7, 0.5, R, stats=True)
+    L = int(K.min())
+    m = st["c"].astype(np.float64) / st["n"]
+    assert (st["t"] >= L - 1e-9).all() and (st["t"] <= m + 1e-9).all()
