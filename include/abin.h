@@ -134,6 +134,31 @@ int abin_wolf(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t
               int32_t mask_format, int32_t h, int32_t w, double k, double R, int32_t L_override, uint32_t flags,
               uint64_t* counters, void* stream);
 
+/* ---- Wolf with the image-adaptive dynamic range (NEXT #3) ------------------
+ * PAPER.md:153 gives Wolf's rule with R; Wolf et al. take R = the maximum of
+ * s over the image (a "two-pass mode").  R = max over the
+ * page of s (each s by the canonical double sequence), or +inf when every
+ * window is constant (then s / R = 0: DESIGN.md reading R21); then Wolf with
+ * that R (and L as abin_wolf).  The mask equals the oracle's bit for bit.
+ * Synchronises `stream` once (R is read back to the host); *R_out (host,
+ * optional) receives R.  Windows within the v5 kernel's domain (abin_max_s). */
+int abin_wolf_adaptive(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out, int64_t out_pitch,
+                       int32_t mask_format, int32_t h, int32_t w, double k, int32_t L_override, uint32_t flags,
+                       uint64_t* counters, double* R_out, void* stream);
+
+/* Max of s over a band's own rows [row0, row0 + H_band) of an image of height
+ * H_global (band geometry as abin_binarize_band: `in` points at the first held
+ * row, global row row0 - halo_top, and the halos hold the rows the windows
+ * reach; a whole image is row0 = 0, H_global = H_band, halos 0).  Exact: the
+ * canonical double s of the maximising pixel (the fp32 filter's variance
+ * selects the candidates within twice its certified error, k_fixup evaluates
+ * them exactly).  *max_s (host) receives the value; synchronises `stream`.
+ * ABIN_ERANGE outside the v5 kernel's window domain (h <= 129, w <= 127) or
+ * for rows TMA cannot stage (base / pitch not multiples of 16) beyond the
+ * re-pitch copy.  The multi-GPU driver all-reduces it (MAX) over the bands. */
+int abin_max_s(const uint8_t* in, int64_t H_band, int64_t W, int64_t in_pitch, int64_t row0, int64_t H_global,
+               int32_t halo_top, int32_t halo_bot, int32_t h, int32_t w, double* max_s, void* stream);
+
 /* ---- Local quantile threshold -------------------------------
  * q in (0, 1]: Q = rho-th smallest in-bounds level, rho = max(1, ceil(q n)).
  * q = 0.5 is the (lower) local median. */

@@ -5,5 +5,5 @@ include/abin.h); this package is its thin Python binding plus the multi-GPU
 driver.  Import fails loudly when the CUDA library has not been built.
 """
 from . import abin  # noqa: F401  (raises ImportError if libabin.so is missing)
-from .abin import (bernsen, binarize_band, binarize_batched, binarize_rule, global_min, niblack, otsu, quantile, sauvola, stats,  # noqa: F401
-                   version, wolf)
+from .abin import (bernsen, binarize_band, binarize_batched, binarize_rule, global_min, max_s, niblack, otsu,  # noqa: F401
+                   probe_filter, quantile, sauvola, stats, version, wolf, wolf_adaptive)

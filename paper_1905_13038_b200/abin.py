@@ -48,6 +48,8 @@ _lib.abin_binarize_band.argtypes = [_I32, _P, _I64, _I64, _I64, _I64, _I64, _I32
                                     _D, _D, _I32, _U32, _P, _P]
 _lib.abin_global_min.argtypes = [_P, _I64, _I64, _I64, _I64, _I64, _P, _P]
 _lib.abin_stats.argtypes = [_I32, _P, _I64, _I64, _I64, _I32, _I32, _D, _D, _I32, _P, _P, _P, _P, _P, _P]
+_lib.abin_max_s.argtypes = [_P, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _I32, _P, _P]
+_lib.abin_wolf_adaptive.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _D, _I32, _U32, _P, _P, _P]
 _lib.abin_probe_filter.argtypes = [_I32, _D, _D, _D, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P]
 _lib.abin_strerror.argtypes = [ctypes.c_int]
 _lib.abin_strerror.restype = ctypes.c_char_p
@@ -65,7 +67,7 @@ _lib.abin_limits.argtypes = [ctypes.POINTER(AbinLimits)]
 EXPORTED = ["abin_sauvola", "abin_niblack", "abin_wolf", "abin_quantile", "abin_bernsen", "abin_binarize_rule", "abin_otsu",
             "abin_binarize_batched",
             "abin_binarize_band", "abin_global_min", "abin_stats", "abin_limits", "abin_strerror", "abin_version",
-            "abin_last_cuda_error", "abin_probe_filter"]
+            "abin_last_cuda_error", "abin_probe_filter", "abin_max_s", "abin_wolf_adaptive"]
 
 
 class AbinError(RuntimeError):
@@ -226,6 +228,33 @@ def global_min(pages: torch.Tensor, stream=None) -> torch.Tensor:
     L = torch.empty(P, dtype=torch.uint8, device=pages.device)
     _check(_lib.abin_global_min(_ptr(pages), pages.stride(0), P, H, W, pages.stride(1), _ptr(L), _stream(stream)))
     return L
+
+
+def max_s(img: torch.Tensor, h: int, w: int, row0: int = 0, H_global: int = None, halo_top: int = 0,
+          halo_bot: int = 0, stream=None) -> float:
+    """Max over the (band's own rows of the) image of the canonical s: Wolf's
+    adaptive R source (R21).  `img` holds halo_top + own + halo_bot rows."""
+    _img2d(img)
+    Hb = img.shape[0] - halo_top - halo_bot
+    out = ctypes.c_double()
+    _check(_lib.abin_max_s(_ptr(img), Hb, img.shape[1], img.stride(0), row0, H_global if H_global else Hb,
+                           halo_top, halo_bot, h, w, ctypes.byref(out), _stream(stream)))
+    return out.value
+
+
+def wolf_adaptive(img: torch.Tensor, h: int, w: int, k: float = 0.5, L: int = -1, packed: bool = False, out=None,
+                  flags: int = 0, counters: torch.Tensor = None, stream=None):
+    """Wolf with R = max s over the image (+inf if every window is constant);
+    returns (mask, R).  One host synchronisation."""
+    _img2d(img)
+    H, W = img.shape
+    if out is None:
+        out = torch.empty((H, (W + 7) // 8 if packed else W), dtype=torch.uint8, device=img.device)
+    R = ctypes.c_double()
+    _check(_lib.abin_wolf_adaptive(_ptr(img), H, W, img.stride(0), _ptr(out), out.stride(0),
+                                   MASK_BITS if packed else MASK_U8, h, w, k, L, flags, _ptr(counters),
+                                   ctypes.byref(R), _stream(stream)))
+    return out, R.value
 
 
 def probe_filter(method: str, c: torch.Tensor, d: torch.Tensor, ncol: torch.Tensor, nrow: torch.Tensor,

@@ -320,6 +320,8 @@ struct MomCall {
   uint8_t* mask_out;
   // Table 1 rules (methods 5..8): parameters, see abin.h
   double rprm[5];
+  // M_MAXS (Wolf's adaptive R): per-page max s as double bits (device)
+  unsigned long long* smax_out;
 };
 
 // Row bands: pick the band count so that the tile count fills whole waves
@@ -606,6 +608,38 @@ int run_moments(const MomCall& c) {
       q.q_count = qcount;
       q.q_cap = cap;
       const int64_t n_tiles = (int64_t)q.n_strips * q.n_bands * c.n_pages;
+      if (c.method == M_MAXS) {
+        // Wolf's adaptive R (R21): pass 0 = max v~ per page, pass 1 = the
+        // pixels within 2 |v~ - v| of it (the true maximum is among them),
+        // then their exact s (k_fixup, canonical double sequence)
+        if (!use_v5 || may_overflow) {
+          cudaFreeAsync(queue, c.stream);
+          return ABIN_ERANGE;
+        }
+        uint32_t* vmax = nullptr;
+        CK(cudaMallocAsync(&vmax, (size_t)c.n_pages * 4, c.stream));
+        CK(cudaMemsetAsync(vmax, 0, (size_t)c.n_pages * 4, c.stream));
+        CK(cudaMemsetAsync(c.smax_out, 0, (size_t)c.n_pages * 8, c.stream));
+        q.vmax_bits = vmax;
+        q.smax_bits = c.smax_out;
+        q.maxs_margin = 2.05f * q.rdv;
+        q.maxs_pass = 0;
+        rc = launch_v5_any(w32, map4, q, n_tiles, c.stream);
+        q.maxs_pass = 1;
+        if (rc == ABIN_OK) rc = launch_v5_any(w32, map4, q, n_tiles, c.stream);
+        if (rc == ABIN_OK) {
+          const size_t fsm = fixup_smem_bytes(win.w);
+          if (fsm > 48 * 1024) CK(cudaFuncSetAttribute(k_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+          int per_sm = 0;
+          CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fixup, kFixNT, fsm));
+          k_fixup<<<num_sms() * std::max(1, per_sm), kFixNT, fsm, c.stream>>>(q);
+          CK(cudaGetLastError());
+        }
+        cudaError_t e1 = cudaFreeAsync(vmax, c.stream), e2 = cudaFreeAsync(queue, c.stream);
+        if (rc == ABIN_OK && e1 != cudaSuccess) return cuda_fail(e1);
+        if (rc == ABIN_OK && e2 != cudaSuccess) return cuda_fail(e2);
+        return rc;
+      }
       rc = use_v5 ? launch_v5_any(w32, map4, q, n_tiles, c.stream) : launch_v4_any(w32, d64, map4, q, n_tiles, c.stream);
       if (rc == ABIN_OK) {
         const size_t fsm = fixup_smem_bytes(win.w);
@@ -678,8 +712,11 @@ int check_params(int32_t method, double p0, double p1) {
   if (method == ABIN_QUANTILE) return (std::isfinite(p0) && p0 > 0.0 && p0 <= 1.0) ? ABIN_OK : ABIN_EINVAL;
   if (method == ABIN_BERNSEN) return std::isfinite(p0) ? ABIN_OK : ABIN_EINVAL;  // contrast (< 0: plain midrange)
   if (!std::isfinite(p0)) return ABIN_EINVAL;
-  if (method == ABIN_SAUVOLA || method == ABIN_WOLF)
+  if (method == ABIN_SAUVOLA)
     if (!std::isfinite(p1) || !(p1 > 0.0)) return ABIN_EINVAL;
+  // Wolf: R > 0, or +inf (s / R = 0: the adaptive R of an all-constant page, R21)
+  if (method == ABIN_WOLF)
+    if (std::isnan(p1) || !(p1 > 0.0)) return ABIN_EINVAL;
   return ABIN_OK;
 }
 
@@ -1218,6 +1255,51 @@ int abin_stats(int32_t method, const uint8_t* in, int64_t H, int64_t W, int64_t 
   cudaError_t f = cudaFreeAsync(scratch, st);
   if (rc == ABIN_OK && f != cudaSuccess) return cuda_fail(f);
   return rc;
+}
+
+int abin_max_s(const uint8_t* in, int64_t H_band, int64_t W, int64_t in_pitch, int64_t row0, int64_t H_global,
+               int32_t halo_top, int32_t halo_bot, int32_t h, int32_t w, double* max_s, void* stream) {
+  if (!in || !max_s || H_band < 1 || W < 1 || h < 1 || w < 1 || in_pitch < W) return ABIN_EINVAL;
+  if (H_band > kMaxDim || W > kMaxDim || H_global > kMaxDim) return ABIN_ERANGE;
+  if (row0 < 0 || H_global < row0 + H_band || halo_top < 0 || halo_bot < 0) return ABIN_EINVAL;
+  const int64_t o = (h + 1) / 2, u = h / 2;
+  // the band must hold every in-image row its windows reach (as abin_binarize_band)
+  if (halo_top < std::min<int64_t>(o - 1, row0) || halo_bot < std::min<int64_t>(u, H_global - row0 - H_band))
+    return ABIN_EINVAL;
+  if (row0 - halo_top < 0 || row0 + H_band + halo_bot > H_global) return ABIN_EINVAL;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  unsigned long long* dmax = nullptr;
+  CK(cudaMallocAsync(&dmax, 8, st));
+  MomCall m;
+  memset(&m, 0, sizeof(m));
+  m.method = M_MAXS; m.in = in; m.buf_rows = H_band + halo_top + halo_bot; m.buf_row0 = row0 - halo_top;
+  m.n_pages = 1; m.W = W; m.in_pitch = in_pitch; m.row0 = row0; m.H_out = H_band; m.H_global = H_global;
+  m.out = nullptr; m.out_pitch = W; m.fmt = ABIN_MASK_U8; m.h = h; m.w = w; m.k = 0.0; m.R = 1.0;
+  m.L_override = 0; m.stream = st; m.smax_out = dmax;
+  int rc = run_moments(m);
+  unsigned long long bits = 0;
+  if (rc == ABIN_OK) {
+    cudaError_t e = cudaMemcpyAsync(&bits, dmax, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_fail(e);
+  }
+  cudaFreeAsync(dmax, st);
+  if (rc == ABIN_OK) memcpy(max_s, &bits, 8);
+  return rc;
+}
+
+int abin_wolf_adaptive(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out, int64_t out_pitch,
+                       int32_t mask_format, int32_t h, int32_t w, double k, int32_t L_override, uint32_t flags,
+                       uint64_t* counters, double* R_out, void* stream) {
+  int rc = check_common(in, H, W, in_pitch, out, out_pitch, mask_format, h, w);
+  if (rc) return rc;
+  if (!std::isfinite(k) || L_override > 255) return ABIN_EINVAL;
+  double ms = 0.0;
+  if ((rc = abin_max_s(in, H, W, in_pitch, 0, H, 0, 0, h, w, &ms, stream))) return rc;
+  const double R = ms > 0.0 ? ms : INFINITY;  // all windows constant: s / R = 0 (R21)
+  if (R_out) *R_out = R;
+  return abin_binarize_batched(ABIN_WOLF, in, 0, out, 0, 1, H, W, in_pitch, out_pitch, mask_format, h, w, k, R,
+                               L_override, flags, counters, stream);
 }
 
 int abin_probe_filter(int32_t method, double k, double R, double L, const uint32_t* c, const uint32_t* d,

@@ -144,6 +144,17 @@ static __global__ void __launch_bounds__(kFixNT, 4) k_fixup(const MomParams p) {
       const uint64_t c = acc, d = dsum;
       const int64_t ncol = min(j + p.r, p.W - 1) - max(j - p.l, (int64_t)-1);
       const uint32_t n = (uint32_t)((a1 - a0 + 1) * ncol);
+      if (p.method == M_MAXS) {
+        // Wolf's adaptive R (R21): the pixel's s by the canonical double
+        // sequence (Alg. 1 l.121-122, as threshold_fp64 and the oracle), into
+        // the page's maximum (non-negative doubles order as their bits)
+        const double nd = (double)n;
+        const double mm = __ddiv_rn((double)c, nd);
+        double v = __dsub_rn(__ddiv_rn((double)d, nd), __dmul_rn(mm, mm));
+        if (v < 0.0) v = 0.0;
+        atomicMax(p.smax_bits + page, (unsigned long long)__double_as_longlong(__dsqrt_rn(v)));
+        continue;
+      }
       const float Lf = (p.method == M_WOLF) ? (float)(p.L_fixed >= 0 ? p.L_fixed : (int)p.L_page[page]) : 0.0f;
       ++st2;
       // stage 2: exact V = n d - c^2 >= 0, fp32 with the tight bound delta2

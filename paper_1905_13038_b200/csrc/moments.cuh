@@ -35,7 +35,7 @@
 
 namespace abin {
 
-enum { M_SAUVOLA = 0, M_NIBLACK = 1, M_WOLF = 2 };
+enum { M_SAUVOLA = 0, M_NIBLACK = 1, M_WOLF = 2, M_MAXS = 3 /* Wolf's adaptive R: max s (v5 + fixup) */ };
 
 struct MomParams {
   int64_t W;          // image width
@@ -76,6 +76,14 @@ struct MomParams {
   const uint32_t* ovf_count;
   uint32_t ovf_cap;
   int32_t n_pages_v4;        // v4: pages of the launch
+  // M_MAXS (Wolf's image-adaptive R = max s, R21): pass 0 reduces the
+  // fp32 v~ per page into vmax_bits; pass 1 queues the pixels whose v~ is within
+  // maxs_margin (>= 2 |v~ - v| bound) of it; k_fixup takes their exact fp64 s
+  // into smax_bits (double bits; s >= 0, so they order as unsigned integers)
+  uint32_t* vmax_bits;
+  unsigned long long* smax_bits;
+  int32_t maxs_pass;
+  float maxs_margin;
   // statistics mode (page 0 only)
   uint64_t* c_out;
   uint64_t* d_out;

@@ -383,6 +383,10 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
   // (halo lanes k < m point below the row: into the ring, read but unused)
   const uint4* lrow0 = pub + (lane - mW);
 
+  // M_MAXS: pass 0 keeps the lane's smallest -v~; pass 1 selects v~ >= vthr
+  float vbest = __int_as_float(0x7f800000);
+  const float vthr = (METHOD == M_MAXS && p.maxs_pass == 1)
+                         ? __int_as_float((int)p.vmax_bits[page]) - p.maxs_margin : 0.0f;
   // ---- main rows
   int q = 0;
   for (int s = WS; s < total; ++s) {
@@ -468,6 +472,7 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
       f2 nb = mul2(nu, splat(-8388608.0f));                   // -2^23 nu (exact)
       uint32_t wv[4];
       float emin = __int_as_float(0x7f800000), smin = emin;
+      uint32_t amb_m = 0u;  // M_MAXS pass 1: pixels within the margin of the page's max v~
       uint4 L = lrow0[(RHO >> 1) * 32];
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
@@ -500,6 +505,22 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
           const f2 I = add2(pk(__uint_as_float(__byte_perm(wd, kMagic, 0x7504u | ((uint32_t)h2 << 4))),
                                __uint_as_float(__byte_perm(wd, kMagic, 0x7504u | ((uint32_t)(h2 + 1) << 4)))),
                             M32);
+          if (METHOD == M_MAXS) {
+            // v~ = q~ - m~^2 (the filter's own variance, |v~ - v| <= dv)
+            const f2 mn = fma2(pk(__uint_as_float(cq[0]), __uint_as_float(cq[1])), nu, nb);
+            const f2 wv = fma2(mn, mn, mul2(pk((float)dq[0], (float)dq[1]), nu));  // -v~
+            const bool va = (vmask >> t0) & 1u, vb = (vmask >> (t0 + 1)) & 1u;
+            const float xa = va ? lo(wv) : __int_as_float(0x7f800000), xb = vb ? hi(wv) : __int_as_float(0x7f800000);
+            if (p.maxs_pass == 0) {
+              emin = fmin3(emin, xa, xb);                       // min of -v~ = -(max v~)
+            } else {
+              amb_m |= (-xa >= vthr ? 1u : 0u) << t0;
+              amb_m |= (-xb >= vthr ? 1u : 0u) << (t0 + 1);
+            }
+            e4[h2] = e4[h2 + 1] = 0.0f;
+            (void)I;
+            continue;
+          }
           f2 sv;
           const f2 e = residual_pair<METHOD>(cq[0], cq[1], dq[0], dq[1], nu, nb, I, fa2, fb2, Lf2, sv);
           emin = fmin3(emin, fabsf(lo(e)), fabsf(hi(e)));
@@ -511,6 +532,15 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
         const uint32_t lo = prmt_sign(__float_as_uint(e4[0]), __float_as_uint(e4[1]), 0x00FBu);
         const uint32_t hi = prmt_sign(__float_as_uint(e4[2]), __float_as_uint(e4[3]), 0xFB00u);
         wv[g] = ~__byte_perm(lo, hi, 0x7610u) & 0x01010101u;
+      }
+      if (METHOD == M_MAXS) {
+        if (p.maxs_pass == 0) {
+          vbest = fminf(vbest, emin);
+        } else if (amb_m) {
+          const uint32_t slot = atomicAdd(p.q_count, 1u);
+          if (slot < p.q_cap) p.q_data[slot] = make_uint4((uint32_t)page, (uint32_t)(i - p.row0), (uint32_t)j0, amb_m);
+        }
+        continue;  // no mask
       }
       // ambiguous lane: a pixel within the certified bound.  Niblack re-tests
       // with the data-dependent bound at its smallest s~ (v4 refined_bound)
@@ -542,6 +572,13 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
       optr += out_pitch;
     }
     stage_end(s);
+  }
+  if (METHOD == M_MAXS && p.maxs_pass == 0) {
+    // max v~ of the tile (>= 0: a clamp at 0 keeps the float bits ordered)
+    float vb = vbest;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) vb = fminf(vb, __shfl_xor_sync(0xffffffffu, vb, off));
+    if (lane == 0 && vb < __int_as_float(0x7f800000)) atomicMax(p.vmax_bits + page, __float_as_uint(fmaxf(-vb, 0.0f)));
   }
 }
 

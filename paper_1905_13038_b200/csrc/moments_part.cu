@@ -66,6 +66,7 @@ template <int W32>
 cudaError_t launch_v5(const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st) {
   if (p.method == M_SAUVOLA) return launch_v5_m<W32, M_SAUVOLA>(map, p, n_tiles, st);
   if (p.method == M_NIBLACK) return launch_v5_m<W32, M_NIBLACK>(map, p, n_tiles, st);
+  if (p.method == M_MAXS) return launch_v5_m<W32, M_MAXS>(map, p, n_tiles, st);
   return launch_v5_m<W32, M_WOLF>(map, p, n_tiles, st);
 }
 

@@ -217,3 +217,25 @@ def global_min_bands(band: Band, group=None, local_min=None) -> int:
     if dist.is_available() and dist.is_initialized():
         dist.all_reduce(L, op=dist.ReduceOp.MIN, group=group)
     return int(L.item())
+
+
+def global_max_s_bands(band: Band, h: int, w: int, group=None, local_max_s=None) -> float:
+    """Wolf's image-adaptive R over the whole banded image (NEXT #3, DESIGN.md
+    R21): the maximum of s over the band's own rows (the windows reach into
+    the halos, which must have been exchanged), then an all-reduce MAX; +inf
+    when every window of the image is constant.  `local_max_s(held, row0, H,
+    top, bot, h, w)` defaults to the device path (abin.max_s); the CPU tests
+    pass a host stand-in to exercise the collective over gloo."""
+    if local_max_s is None:
+        from . import abin
+
+        def local_max_s(held, row0, H, top, bot, h_, w_):
+            return abin.max_s(held, h_, w_, row0=row0, H_global=H, halo_top=top, halo_bot=bot)
+    held = band.buf[0:band.top + (band.r1 - band.r0) + band.bot]
+    m = torch.tensor([float(local_max_s(held, band.r0, band.H, band.top, band.bot, h, w))], dtype=torch.float64)
+    if band.buf.is_cuda:
+        m = m.to(band.buf.device)
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
+    v = float(m.item())
+    return v if v > 0.0 else float("inf")

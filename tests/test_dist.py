@@ -127,3 +127,40 @@ def test_band_decomposition_with_halo_exchange(tmp_path, world, H, W, h, w, meth
 def test_band_too_small_for_halo():
     with pytest.raises(ValueError):
         adist.make_band(20, 16, 31, 1, 2, device="cpu")
+
+
+def _max_s_worker(rank, world, port, H, W, h, w, result_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        img = synth.page(H, W, synth.config_seed(4, 9), stain=True)
+        band = adist.make_band(H, W, h, rank, world, device="cpu")
+        band.own.copy_(torch.from_numpy(img[band.r0:band.r1]))
+        for wk in adist.exchange_halos(band, rank, world, h):
+            wk.wait()
+
+        def host_max_s(held, row0, H_, top, bot, h_, w_):
+            # the oracle's per-pixel c, d, n on the held rows (the windows of the
+            # own rows stay inside them), then the canonical double s
+            st = oracle.binarize("sauvola", np.ascontiguousarray(held.numpy()), h_, w_, 0.5, 128.0, stats=True)
+            own = slice(top, held.shape[0] - bot)
+            c, d, n = (st[k][own].astype(np.float64) for k in ("c", "d", "n"))
+            m = c / n
+            v = np.maximum(d / n - m * m, 0.0)
+            return float(np.sqrt(v).max())
+
+        R = adist.global_max_s_bands(band, h, w, local_max_s=host_max_s)
+        if rank == 0:
+            np.save(result_path, np.array([R]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_adaptive_R_all_reduce_over_bands(tmp_path, world):
+    H, W, h, w = 46, 31, 9, 7
+    path = str(tmp_path / "R.npy")
+    mp.start_processes(_max_s_worker, args=(world, _free_port(), H, W, h, w, path), nprocs=world, join=True,
+                       start_method="spawn")
+    img = synth.page(H, W, synth.config_seed(4, 9), stain=True)
+    assert float(np.load(path)[0]) == oracle.adaptive_R(img, h, w)
