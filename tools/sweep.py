@@ -84,3 +84,6 @@ for rule in ("feng", "rais", "khurshid", "phansalkar"):
     print(json.dumps({"next": rule, "ms": ms, "gpx_s": 7016 * 4960 / ms / 1e6}), flush=True)
 ms = timed(lambda k: ab.otsu(x[k, 0]), nr, reps=5)
 print(json.dumps({"next": "otsu", "ms": ms, "gpx_s": 7016 * 4960 / ms / 1e6}), flush=True)
+# NEXT #3: Wolf with the adaptive R (max s: two v5 passes + exact candidates; one host sync per page)
+ms = timed(lambda k: ab.wolf_adaptive(x[k, 0], 61, 61, 0.5), nr, reps=5)
+print(json.dumps({"next": "wolf_adaptive", "ms": ms, "gpx_s": 7016 * 4960 / ms / 1e6}), flush=True)
