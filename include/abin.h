@@ -183,9 +183,14 @@ int abin_bernsen(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint
  *   ABIN_KHURSHID    {k, N_mode}: t = m + k sqrt(s^2 + m^2 (N - 1)/N), N = h w (N_mode = 0) or the
  *                    clamped count n (N_mode != 0)
  *   ABIN_PHANSALKAR  {k, R, p, q}: t = m (1 + p e^(-q m) + k (s/R - 1))
- * Every pixel is decided in IEEE double (left-to-right evaluation; pow/exp are
- * the device's double routines, <= 2 ulp).  ABIN_EINVAL for an unknown rule,
- * missing or non-finite params, R <= 0. */
+ * The mask is the IEEE-double decision of every pixel (left-to-right
+ * evaluation; pow/exp are the device's double routines, <= 2 ulp).  Feng,
+ * Rais, Phansalkar with q < 0 and windows beyond h <= 129, w <= 127 compute it
+ * per pixel (v3 kernel); Khurshid and Phansalkar with q >= 0 take the v5
+ * kernel's certified fp32 filter (exact integer window sums, a bound on the
+ * fp32 residual derived per parameter set) and decide
+ * in double only the pixels inside the bound -- the same mask.  ABIN_EINVAL
+ * for an unknown rule, missing or non-finite params, R <= 0. */
 int abin_binarize_rule(int32_t rule, const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out,
                        int64_t out_pitch, int32_t mask_format, int32_t h, int32_t w, const double* params,
                        int32_t n_params, uint32_t flags, uint64_t* counters, void* stream);
@@ -250,14 +255,19 @@ int abin_stats(int32_t method, const uint8_t* in, int64_t H, int64_t W, int64_t 
  * d < 2^32), ncol, nrow the window's column / row counts (n = ncol nrow,
  * PAPER.md:118), I the centre pixel -- all device arrays of `count` entries;
  * e_out (device, count floats) receives e~, s_out (optional) s~.  method is
- * 0..2 (Sauvola, Niblack, Wolf with global minimum L).  bounds (optional,
- * host, 5 doubles) receives the certified bound: [0] the coarse bound the
- * kernel tests |e~| against, [1..4] rb0, rb1, rdv, rsdv of the data-dependent
- * bound rb0 + rb1 min(rsdv, rdv / s~) (used for Niblack).  The claim the tests
- * check: |e~ - e*| <= bound for the exact e* = I - t(c, d, n).  Asynchronous on
- * `stream`; ABIN_EINVAL on bad arguments. */
-int abin_probe_filter(int32_t method, double k, double R, double L, const uint32_t* c, const uint32_t* d,
-                      const uint32_t* ncol, const uint32_t* nrow, const uint8_t* I, int64_t count, float* e_out,
+ * 0..2 (Sauvola, Niblack, Wolf with global minimum L; rule_params unused, may
+ * be NULL) or the v5 rules 7 (Khurshid: rule_params = {k, N_mode, h w}) and
+ * 8 (Phansalkar: rule_params = {k, R, p, q}, q >= 0; k, R arguments unused);
+ * ABIN_ERANGE for a rule parameter set the v5 kernel does not take (those run
+ * on the exact path).  bounds (optional, host, 5 doubles) receives the
+ * certified bound: [0] the coarse bound the kernel tests |e~| against,
+ * [1..4] rb0, rb1, rdv, rsdv of the data-dependent bound
+ * rb0 + rb1 min(rsdv, rdv / s~) (used for Niblack and Khurshid).  The claim
+ * the tests check: |e~ - e*| <= bound for the exact e* = I - t(c, d, n).
+ * Asynchronous on `stream`; ABIN_EINVAL on bad arguments. */
+int abin_probe_filter(int32_t method, double k, double R, double L, const double* rule_params, const uint32_t* c,
+                      const uint32_t* d, const uint32_t* ncol, const uint32_t* nrow, const uint8_t* I, int64_t count,
+                      float* e_out,
                       float* s_out, double* bounds, void* stream);
 
 /* ---- Limits, versions, errors ------------------------------------------------ */

@@ -50,7 +50,7 @@ _lib.abin_global_min.argtypes = [_P, _I64, _I64, _I64, _I64, _I64, _P, _P]
 _lib.abin_stats.argtypes = [_I32, _P, _I64, _I64, _I64, _I32, _I32, _D, _D, _I32, _P, _P, _P, _P, _P, _P]
 _lib.abin_max_s.argtypes = [_P, _I64, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _I32, _P, _P]
 _lib.abin_wolf_adaptive.argtypes = [_P, _I64, _I64, _I64, _P, _I64, _I32, _I32, _I32, _D, _I32, _U32, _P, _P, _P]
-_lib.abin_probe_filter.argtypes = [_I32, _D, _D, _D, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P]
+_lib.abin_probe_filter.argtypes = [_I32, _D, _D, _D, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P]
 _lib.abin_strerror.argtypes = [ctypes.c_int]
 _lib.abin_strerror.restype = ctypes.c_char_p
 _lib.abin_version.restype = ctypes.c_char_p
@@ -258,15 +258,21 @@ def wolf_adaptive(img: torch.Tensor, h: int, w: int, k: float = 0.5, L: int = -1
 
 
 def probe_filter(method: str, c: torch.Tensor, d: torch.Tensor, ncol: torch.Tensor, nrow: torch.Tensor,
-                 I: torch.Tensor, k: float, R: float = 128.0, L: float = 0.0, stream=None):
+                 I: torch.Tensor, k: float = 0.0, R: float = 128.0, L: float = 0.0, rule_params=None, stream=None):
     """Test hook: the kernel's fp32 residuals e~ = I - t~ (and s~) for tuples
     of exact window data (uint32 c, d, ncol, nrow; uint8 I, all on the device)
-    and the certified bound [coarse, rb0, rb1, rdv, rsdv] (abin.h)."""
+    and the certified bound [coarse, rb0, rb1, rdv, rsdv] (abin.h).  Rules
+    "khurshid" / "phansalkar" take rule_params ({k, N_mode, h w} /
+    {k, R, p, q})."""
     n = c.numel()
     e = torch.empty(n, dtype=torch.float32, device=c.device)
     sv = torch.empty(n, dtype=torch.float32, device=c.device)
     b = (ctypes.c_double * 5)()
-    _check(_lib.abin_probe_filter(METHODS[method], k, R, L, _ptr(c), _ptr(d), _ptr(ncol), _ptr(nrow), _ptr(I), n,
+    code = RULES[method] if method in RULES else METHODS[method]
+    rp = None
+    if rule_params is not None:
+        rp = (ctypes.c_double * 5)(*([float(x) for x in rule_params] + [0.0] * (5 - len(rule_params))))
+    _check(_lib.abin_probe_filter(code, k, R, L, rp, _ptr(c), _ptr(d), _ptr(ncol), _ptr(nrow), _ptr(I), n,
                                   _ptr(e), _ptr(sv), b, _stream(stream)))
     return e, sv, list(b)
 

@@ -213,19 +213,27 @@ FilterConsts filter_consts(int method, double k, double R) {
 // expression.  Counts n lie in [n_min, n_max]; the start value and the
 // relative sums are window sums of windows with counts <= n_max, so they are
 // bounded by 255 n_max (c) and 255^2 n_max (d).
-FilterConsts filter_consts_v5(int method, double k, double R) {
+FilterConsts filter_consts_v5(int method, double k, double R, const double* rprm = nullptr) {
   const double u = std::ldexp(1.0, -24);
   const double eps_sqrt = 8 * u;            // sqrt.approx.f32: relative error < 2^-22 (taken as 2^-21)
   const double eps64 = 1e-6;                // |t_fp64 - t*| (the canonical double sequence)
   const double e_nu = 3.01 * u;             // fl(fl(1/ncol) fl(1/nrow)): three roundings
-  const double qmax = 255.0 * 255.0, smax = 127.5;
+  const double qmax = 255.0 * 255.0;
+  // Khurshid's radicand W = q - m^2 / N lies in [0, 255^2]; the others' v in [0, 127.5^2]
+  const double smax = method == M_KHURSHID ? 255.0 : 127.5;
   const double dm = 255.0 * (e_nu + u) * 1.01;                                // |m~ - m|: one rounding of c nu~
   const double dq = qmax * (e_nu + 2 * u) * 1.01;                             // |q~ - q|: fl(d), then fl(fl(d) nu~)
-  const double dv = (2 * 255.0 + dm) * dm + dq + 1.01 * u * (smax * smax + 1.0);  // |(-w~) - v|, w~ = fl(m~^2 - q~)
+  double dv = (2 * 255.0 + dm) * dm + dq + 1.01 * u * (smax * smax + 1.0);    // |(-w~) - v|, w~ = fl(m~^2 - q~)
+  if (method == M_KHURSHID)
+    // w~ = fl(m~ fl(m~ iN~) - q~), iN~ = 1/N (1 + e_nu): |m~^2 / N - m^2 / N| <= (510 + dm) dm,
+    // the product's two roundings and iN~'s error <= 255^2 (e_nu + u), then q~ and the last rounding
+    dv = (2 * 255.0 + dm) * dm * 1.01 + qmax * (e_nu + u) * 1.01 + dq + 1.01 * u * (qmax + 1.0);
   const double rv = std::sqrt(dv);
   const double ds = rv + eps_sqrt * (smax + rv);                               // |s~ - s| (coarse)
   FilterConsts f;
   memset(&f, 0, sizeof(f));
+  if (method == M_KHURSHID) k = rprm[0];
+  if (method == M_PHANSALKAR) { k = rprm[0]; R = rprm[1]; }
   auto bound = [&](double dsx) {
     if (method == M_SAUVOLA) {
       const double a = std::fabs(1.0 - k), b = std::fabs(k / R);
@@ -233,7 +241,22 @@ FilterConsts filter_consts_v5(int method, double k, double R) {
       const double dg = b * (dsx + smax * u) + a * u + 1.01 * u * G;           // |g~ - g|
       return dm * G + 255.0 * dg + dm * dg + 1.01 * u * 255.0 * (1.0 + G);
     }
-    if (method == M_NIBLACK) {
+    if (method == M_PHANSALKAR) {
+      // g = (1 - k) + (k/R) s + p E, E = 2^(-q log2(e) m) <= 1 (q >= 0); a~ = fl(fl(q log2 e) (-m~))
+      // has |a~ - a| <= q log2(e) (dm + 2.02 u 255); ex2.approx (relative error eps_ex2, flush
+      // below 2^-126): |E~ - E| <= 2^|da| (ln2 |da| + eps_ex2) + 2^-126, ln2 log2(e) = 1
+      const double pp = std::fabs(rprm[2]), q = rprm[3];
+      const double eps_ex2 = 32 * u;
+      const double da = q * 1.4426950408889634 * (dm + 2.02 * u * 255.0);
+      const double g2 = std::exp2(da);
+      const double dE = g2 * (q * (dm + 2.02 * u * 255.0) + eps_ex2) * 1.01 + std::ldexp(1.0, -126);
+      const double Em = g2 * (1.0 + eps_ex2);
+      const double a = std::fabs(1.0 - k), b = std::fabs(k / R);
+      const double G = a + b * (smax + dsx) + pp * Em;
+      const double dg = b * (dsx + smax * u) + a * u + pp * (dE + u * Em) + 2.02 * u * G;
+      return dm * G + 255.0 * dg + dm * dg + 1.01 * u * 255.0 * (1.0 + G);
+    }
+    if (method == M_NIBLACK || method == M_KHURSHID) {
       const double ak = std::fabs(k);
       return dm + 2.02 * u * 255.0 + ak * dsx + ak * smax * u + 1.01 * u * (510.0 + ak * smax);
     }
@@ -244,11 +267,11 @@ FilterConsts filter_consts_v5(int method, double k, double R) {
     const double db = dsx * iR + smax * iR * u + 1.01 * u * Bm;                 // |b~ - (1 - s/R)|
     return dka * Bm + ak * 255.0 * db + dm + 2.02 * u * 255.0 + 1.01 * u * (510.0 + ak * 255.0 * Bm);
   };
-  if (method == M_SAUVOLA) { f.fa = (float)(1.0 - k); f.fb = (float)(k / R); }
-  else if (method == M_NIBLACK) { f.fa = 0.0f; f.fb = (float)k; }
+  if (method == M_SAUVOLA || method == M_PHANSALKAR) { f.fa = (float)(1.0 - k); f.fb = (float)(k / R); }
+  else if (method == M_NIBLACK || method == M_KHURSHID) { f.fa = 0.0f; f.fb = (float)k; }
   else { f.fa = (float)k; f.fb = (float)(1.0 / R); }
   f.delta1 = (float)(1.25 * (bound(ds) + eps64) + 1e-6);
-  // data-dependent form (Niblack): |s~ - s| <= min(sqrt dv, dv (1 + eps) / s~) + eps (smax + sqrt dv);
+  // data-dependent form (Niblack, Khurshid): |s~ - s| <= min(sqrt dv, dv (1 + eps) / s~) + eps (smax + sqrt dv);
   // bound(ds) is affine in ds
   const double b0 = bound(0.0), b1 = bound(1.0) - b0;
   f.rb0 = (float)((1.25 * (b0 + b1 * eps_sqrt * (smax + rv) + eps64) + 1e-6) * (1 + 1e-6));
@@ -256,6 +279,28 @@ FilterConsts filter_consts_v5(int method, double k, double R) {
   f.rdv = (float)(dv * (1 + eps_sqrt) * (1 + 1e-6));
   f.rsdv = (float)(rv * (1 + 1e-6));
   return f;
+}
+
+// The v5 rules' extra operands (MomParams aux0 / aux1, moments5.cuh aux_operand):
+// Khurshid 1/(h w) (N_mode 0); Phansalkar p and q log2(e)
+void rule_aux_v5(int method, const double* rprm, double hw, float* aux0, float* aux1) {
+  *aux0 = *aux1 = 0.0f;
+  if (method == M_KHURSHID) *aux0 = (float)(1.0 / hw);
+  if (method == M_PHANSALKAR) { *aux0 = (float)rprm[2]; *aux1 = (float)(rprm[3] * 1.4426950408889634); }
+}
+
+// Khurshid and Phansalkar (q >= 0) run on v5 behind the certified filter when
+// its bound is usable (small against the 0.5 spacing of the integer pixels);
+// the other rules and other parameters stay on the exact v3 path
+bool rule_on_v5(int method, const double* rprm, double hw) {
+  if (method != M_KHURSHID && method != M_PHANSALKAR) return false;
+  for (int z = 0; z < 4; ++z)
+    if (!std::isfinite(rprm[z])) return false;
+  if (method == M_PHANSALKAR && !(rprm[3] >= 0.0)) return false;
+  const FilterConsts f = filter_consts_v5(method, 0.0, 1.0, rprm);
+  float a0, a1;
+  rule_aux_v5(method, rprm, hw, &a0, &a1);
+  return std::isfinite(f.delta1) && f.delta1 < 8.0f && std::isfinite(a0) && std::isfinite(a1);
 }
 
 // The device's SM count (cudaDevAttrMultiProcessorCount), cached per device;
@@ -493,7 +538,10 @@ int run_moments(const MomCall& c) {
   // v4 (warp CTAs, certified fp32 + deferred exact fixup) for the production
   // path; the v3 kernel (inline exact path) for rules, statistics, forced fp64
   // and rows TMA cannot stage
-  const bool use_v4 = fast && tma_ok && !(c.flags & ABIN_V3_INTERNAL) && !rule && !stats &&
+  const bool d64_sq = (c.flags & ABIN_FORCE_U64_SQ) || (uint64_t)win.h * (uint64_t)win.w * 65025u >= (1ull << 32);
+  const bool v5_rule = rule && rule_on_v5(c.method, c.rprm, (double)win.h * (double)win.w) && !d64_sq &&
+                       win.h <= v5::kMaxH && win.w <= v5::kMaxW && !(c.flags & ABIN_V4_INTERNAL);
+  const bool use_v4 = fast && tma_ok && !(c.flags & ABIN_V3_INTERNAL) && (!rule || v5_rule) && !stats &&
                       !(c.flags & ABIN_FORCE_FP64);
   CUtensorMap map, map4;
   int rc = encode_map(c, fast ? kR : (nt_wide == 128 ? 8 : 4), tma_ok, &map);
@@ -571,8 +619,9 @@ int run_moments(const MomCall& c) {
       if (use_v5) {
         q.KH = (win.w + kG - 1) / kG;
         q.Tw = kG * (32 - q.KH);
-        const FilterConsts f5 = filter_consts_v5(c.method, c.k, c.R);
+        const FilterConsts f5 = filter_consts_v5(c.method, c.k, c.R, c.rprm);
         q.fa = f5.fa; q.fb = f5.fb; q.delta1 = f5.delta1;
+        rule_aux_v5(c.method, c.rprm, (double)win.h * (double)win.w, &q.aux0, &q.aux1);
         q.rb0 = f5.rb0; q.rb1 = f5.rb1; q.rdv = f5.rdv; q.rsdv = f5.rsdv;
       }
       // one warp per CTA; a strip = one warp's 32 - KH valid lanes
@@ -1302,12 +1351,25 @@ int abin_wolf_adaptive(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch
                                L_override, flags, counters, stream);
 }
 
-int abin_probe_filter(int32_t method, double k, double R, double L, const uint32_t* c, const uint32_t* d,
-                      const uint32_t* ncol, const uint32_t* nrow, const uint8_t* I, int64_t count, float* e_out,
-                      float* s_out, double* bounds, void* stream) {
-  if (method < ABIN_SAUVOLA || method > ABIN_WOLF || count < 0) return ABIN_EINVAL;
-  if (!std::isfinite(k) || !std::isfinite(R) || !(R > 0.0) || !std::isfinite(L)) return ABIN_EINVAL;
-  const FilterConsts f = filter_consts_v5(method, k, R);
+int abin_probe_filter(int32_t method, double k, double R, double L, const double* rule_params, const uint32_t* c,
+                      const uint32_t* d, const uint32_t* ncol, const uint32_t* nrow, const uint8_t* I, int64_t count,
+                      float* e_out, float* s_out, double* bounds, void* stream) {
+  if (count < 0) return ABIN_EINVAL;
+  const bool rule = method == ABIN_KHURSHID || method == ABIN_PHANSALKAR;
+  if (!rule && (method < ABIN_SAUVOLA || method > ABIN_WOLF)) return ABIN_EINVAL;
+  float aux0 = 0.0f, aux1 = 0.0f;
+  int nmode = 0;
+  if (rule) {
+    if (!rule_params) return ABIN_EINVAL;
+    nmode = method == ABIN_KHURSHID && rule_params[1] != 0.0;
+    const double hw = method == ABIN_KHURSHID && !nmode ? rule_params[2] : 1.0;  // Khurshid's N = h w
+    if (!(hw >= 1.0)) return ABIN_EINVAL;
+    if (!rule_on_v5(method, rule_params, hw)) return ABIN_ERANGE;  // not a parameter set v5 takes
+    rule_aux_v5(method, rule_params, hw, &aux0, &aux1);
+  } else if (!std::isfinite(k) || !std::isfinite(R) || !(R > 0.0) || !std::isfinite(L)) {
+    return ABIN_EINVAL;
+  }
+  const FilterConsts f = filter_consts_v5(method, k, R, rule_params);
   if (bounds) {
     bounds[0] = f.delta1; bounds[1] = f.rb0; bounds[2] = f.rb1; bounds[3] = f.rdv; bounds[4] = f.rsdv;
   }
@@ -1316,9 +1378,14 @@ int abin_probe_filter(int32_t method, double k, double R, double L, const uint32
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const unsigned nb = (unsigned)((count + 255) / 256);
   const float Lf = (float)L;
-  if (method == M_SAUVOLA) v5::k_probe<M_SAUVOLA><<<nb, 256, 0, st>>>(c, d, ncol, nrow, I, count, f.fa, f.fb, Lf, e_out, s_out);
-  else if (method == M_NIBLACK) v5::k_probe<M_NIBLACK><<<nb, 256, 0, st>>>(c, d, ncol, nrow, I, count, f.fa, f.fb, Lf, e_out, s_out);
-  else v5::k_probe<M_WOLF><<<nb, 256, 0, st>>>(c, d, ncol, nrow, I, count, f.fa, f.fb, Lf, e_out, s_out);
+#define ABIN_PROBE(M) \
+  v5::k_probe<M><<<nb, 256, 0, st>>>(c, d, ncol, nrow, I, count, f.fa, f.fb, Lf, aux0, aux1, nmode, e_out, s_out)
+  if (method == M_SAUVOLA) ABIN_PROBE(M_SAUVOLA);
+  else if (method == M_NIBLACK) ABIN_PROBE(M_NIBLACK);
+  else if (method == M_WOLF) ABIN_PROBE(M_WOLF);
+  else if (method == M_KHURSHID) ABIN_PROBE(M_KHURSHID);
+  else ABIN_PROBE(M_PHANSALKAR);
+#undef ABIN_PROBE
   CK(cudaGetLastError());
   return ABIN_OK;
 }

@@ -14,6 +14,7 @@
 #include <cstdint>
 
 #include "moments.cuh"
+#include "rules.cuh"
 
 namespace abin {
 
@@ -29,6 +30,24 @@ __host__ __device__ inline int fixup_chunks(int w) { return (15 + w + 15 + 15) /
 __host__ __device__ inline int fixup_stage_bytes(int w) { return (32 * (4 * fixup_chunks(w) + 1) * 4 + 15) & ~15; }
 __host__ __device__ inline int fixup_warp_bytes(int w) { return fixup_stage_bytes(w) + 32 * 16 * (8 + 4); }
 inline size_t fixup_smem_bytes(int w) { return (size_t)kFixWarps * fixup_warp_bytes(w); }
+
+// One exact decision into the output: a byte, or the MSB-first bit j of the
+// row patched with a 32-bit atomic on the aligned word holding its byte (the
+// word's other bytes -- possibly of a neighbouring row -- are left as they
+// are; CUDA allocations are 256-byte aligned, so the word never leaves the
+// allocation)
+__device__ __forceinline__ void store_mask(const MomParams& p, int page, int64_t y, int64_t j, uint32_t mk) {
+  uint8_t* orow = p.out + (int64_t)page * p.out_page_stride + y * p.out_pitch;
+  if (p.fmt == 0) {
+    orow[j] = (uint8_t)mk;
+  } else {
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(orow + (j >> 3));
+    unsigned int* word = reinterpret_cast<unsigned int*>(addr & ~(uintptr_t)3);
+    const unsigned int bit = 1u << (8 * (unsigned)(addr & 3) + (7 - (unsigned)(j & 7)));
+    if (mk) atomicOr(word, bit);
+    else atomicAnd(word, ~bit);
+  }
+}
 
 static __global__ void __launch_bounds__(kFixNT, 4) k_fixup(const MomParams p) {
   extern __shared__ __align__(16) uint8_t fsm[];
@@ -155,6 +174,15 @@ static __global__ void __launch_bounds__(kFixNT, 4) k_fixup(const MomParams p) {
         atomicMax(p.smax_bits + page, (unsigned long long)__double_as_longlong(__dsqrt_rn(v)));
         continue;
       }
+      if (is_rule(p.method)) {
+        // v5 rules (Khurshid, Phansalkar): straight to the Table-1 row in IEEE double
+        const double tt = threshold_rule_fp64(p.method, c, d, n, p.rp, 0.0, page);
+        const uint32_t mk = ((double)I <= tt) ? 0u : 1u;
+        ++fb64;
+        if (fabs((double)I - tt) < 1e-9) ++near;
+        store_mask(p, page, q.y, j, mk);
+        continue;
+      }
       const float Lf = (p.method == M_WOLF) ? (float)(p.L_fixed >= 0 ? p.L_fixed : (int)p.L_page[page]) : 0.0f;
       ++st2;
       // stage 2: exact V = n d - c^2 >= 0, fp32 with the tight bound delta2
@@ -173,20 +201,7 @@ static __global__ void __launch_bounds__(kFixNT, 4) k_fixup(const MomParams p) {
         ++fb64;
         if (fabs((double)I - tt) < 1e-9) ++near;
       }
-      uint8_t* orow = p.out + (int64_t)page * p.out_page_stride + (int64_t)q.y * p.out_pitch;
-      if (p.fmt == 0) {
-        orow[j] = (uint8_t)mk;
-      } else {
-        // MSB-first bit j of the row, patched with a 32-bit atomic on the
-        // aligned word holding its byte (the word's other bytes -- possibly of
-        // a neighbouring row -- are left as they are; CUDA allocations are
-        // 256-byte aligned, so the word never leaves the allocation)
-        const uintptr_t addr = reinterpret_cast<uintptr_t>(orow + (j >> 3));
-        unsigned int* word = reinterpret_cast<unsigned int*>(addr & ~(uintptr_t)3);
-        const unsigned int bit = 1u << (8 * (unsigned)(addr & 3) + (7 - (unsigned)(j & 7)));
-        if (mk) atomicOr(word, bit);
-        else atomicAnd(word, ~bit);
-      }
+      store_mask(p, page, q.y, j, mk);
     }
   }
   if (p.counters) {

@@ -43,6 +43,7 @@
 #include "moments.cuh"
 #include "moments4.cuh"
 #include "ptx.cuh"
+#include "rules.cuh"
 
 namespace abin {
 namespace v5 {
@@ -140,7 +141,13 @@ __device__ __forceinline__ float fmin3(float a, float b, float c) {
 // fp32 operations: both go through this function).
 //   mn = -m~, qn = -q~ (pairs), I exact, fa/fb the method constants, Lf (Wolf)
 template <int METHOD>
-__device__ __forceinline__ f2 residual2(f2 mn, f2 qn, f2 I, f2 fa2, f2 fb2, f2 Lf2, f2& s) {
+__device__ __forceinline__ f2 residual2(f2 mn, f2 qn, f2 I, f2 fa2, f2 fb2, f2 Lf2, f2& s, f2 y2 = f2(0)) {
+  if (METHOD == M_KHURSHID) {
+    // t = m + k sqrt(s^2 + m^2 (N-1)/N) = m + k sqrt(q - m^2 / N)   (Lf2 = 1/N)
+    const f2 wk = fma2(mn, mul2(mn, Lf2), qn);  // m^2 / N - q
+    s = pk(sqrt_approx(fabsf(lo(wk))), sqrt_approx(fabsf(hi(wk))));
+    return fma2(fb2, s, add2(I, mn));           // (I - m) - k sqrt(.)   (fb2 = -k)
+  }
   const f2 wv = fma2(mn, mn, qn);  // m^2 - q = -v~
   s = pk(sqrt_approx(fabsf(lo(wv))), sqrt_approx(fabsf(hi(wv))));
   if (METHOD == M_SAUVOLA) {
@@ -148,6 +155,18 @@ __device__ __forceinline__ f2 residual2(f2 mn, f2 qn, f2 I, f2 fa2, f2 fb2, f2 L
     return fma2(mn, g, I);           // I - m g
   } else if (METHOD == M_NIBLACK) {
     return fma2(fb2, s, add2(I, mn));  // (I - m) - k s   (fb2 = -k)
+  } else if (METHOD == M_PHANSALKAR) {
+    // t = m (1 + p e^(-q m) + k (s/R - 1)) = m ((1 - k) + (k/R) s + p e^(-q m)); q >= 0
+    const f2 a = mul2(y2, mn);  // -q m log2(e)   (y2 = q log2(e))
+    f2 E;
+    {
+      float e0, e1;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(lo(a)));
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(hi(a)));
+      E = pk(e0, e1);
+    }
+    const f2 g = fma2(E, Lf2, fma2(s, fb2, fa2));  // (1 - k) + (k/R) s + p E   (Lf2 = p)
+    return fma2(mn, g, I);                         // I - m g
   } else {
     const f2 b = fma2(fb2, s, splat(1.0f));   // 1 - s/R      (fb2 = -1/R)
     const f2 ka = mul2(fa2, add2(mn, Lf2));   // k (m - L)    (fa2 = -k)
@@ -158,8 +177,8 @@ __device__ __forceinline__ f2 residual2(f2 mn, f2 qn, f2 I, f2 fa2, f2 fb2, f2 L
 // the method constants as the packed operands residual2 takes
 template <int METHOD>
 __device__ __forceinline__ void method_consts(float fa, float fb, f2& fa2, f2& fb2) {
-  if (METHOD == M_SAUVOLA) { fa2 = splat(fa); fb2 = splat(fb); }
-  else if (METHOD == M_NIBLACK) { fa2 = splat(0.0f); fb2 = splat(-fb); }
+  if (METHOD == M_SAUVOLA || METHOD == M_PHANSALKAR) { fa2 = splat(fa); fb2 = splat(fb); }
+  else if (METHOD == M_NIBLACK || METHOD == M_KHURSHID) { fa2 = splat(0.0f); fb2 = splat(-fb); }
   else { fa2 = splat(-fa); fb2 = splat(-fb); }
 }
 
@@ -171,10 +190,19 @@ __device__ __forceinline__ void method_consts(float fa, float fb, f2& fa2, f2& f
 // is the correctly rounded c (-1/n); -q~ = fl(fl(d) nu).
 template <int METHOD>
 __device__ __forceinline__ f2 residual_pair(uint32_t cb0, uint32_t cb1, uint32_t d0, uint32_t d1, f2 nu, f2 nb, f2 I,
-                                            f2 fa2, f2 fb2, f2 Lf2, f2& s) {
+                                            f2 fa2, f2 fb2, f2 Lf2, f2& s, f2 y2 = f2(0)) {
   const f2 mn = fma2(pk(__uint_as_float(cb0), __uint_as_float(cb1)), nu, nb);
   const f2 qn = mul2(pk((float)d0, (float)d1), nu);
-  return residual2<METHOD>(mn, qn, I, fa2, fb2, Lf2, s);
+  return residual2<METHOD>(mn, qn, I, fa2, fb2, Lf2, s, y2);
+}
+
+// The rules' extra operands: Khurshid's 1/N (N = h w, or the pixel's n when
+// N_mode != 0: then -nu), Phansalkar's p and q log2(e); Wolf's L
+template <int METHOD>
+__device__ __forceinline__ f2 aux_operand(const MomParams& p, f2 Lf2, f2 nu) {
+  if (METHOD == M_KHURSHID) return p.rp.p[1] != 0.0 ? mul2(nu, splat(-1.0f)) : splat(p.aux0);
+  if (METHOD == M_PHANSALKAR) return splat(p.aux0);
+  return Lf2;
 }
 
 // The filter probe: one tuple (c, d, ncol, nrow, I) per thread, evaluated by
@@ -182,16 +210,21 @@ __device__ __forceinline__ f2 residual_pair(uint32_t cb0, uint32_t cb1, uint32_t
 // bound; the host checks |e~ - e*| <= the bound over many tuples).
 template <int METHOD>
 __global__ void k_probe(const uint32_t* c, const uint32_t* d, const uint32_t* ncol, const uint32_t* nrow,
-                        const uint8_t* I, int64_t count, float fa, float fb, float Lf, float* e_out, float* s_out) {
+                        const uint8_t* I, int64_t count, float fa, float fb, float Lf, float aux0, float aux1,
+                        int nmode, float* e_out, float* s_out) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= count) return;
   const float nu1 = -(__frcp_rn((float)ncol[q]) * __frcp_rn((float)nrow[q]));
   const f2 nu = splat(nu1), nb = mul2(nu, splat(-8388608.0f));
   f2 fa2, fb2;
   method_consts<METHOD>(fa, fb, fa2, fb2);
+  f2 x2 = splat(Lf);
+  if (METHOD == M_KHURSHID) x2 = nmode ? mul2(nu, splat(-1.0f)) : splat(aux0);
+  if (METHOD == M_PHANSALKAR) x2 = splat(aux0);
   const float If = (float)I[q];
   f2 sv;
-  const f2 e = residual_pair<METHOD>(kBias + c[q], kBias + c[q], d[q], d[q], nu, nb, pk(If, If), fa2, fb2, splat(Lf), sv);
+  const f2 e = residual_pair<METHOD>(kBias + c[q], kBias + c[q], d[q], d[q], nu, nb, pk(If, If), fa2, fb2, x2, sv,
+                                     splat(aux1));
   e_out[q] = lo(e);
   if (s_out) s_out[q] = lo(sv);
 }
@@ -374,6 +407,7 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
   f2 fa2, fb2;
   method_consts<METHOD>(p.fa, p.fb, fa2, fb2);
   const f2 Lf2 = splat(Lf);
+  const f2 y2 = splat(p.aux1);  // Phansalkar: q log2(e)
   // interior columns: ncol = w; per-row -1/n = -(1/w)(1/nrow) computed once per row
   const float inv_w = __frcp_rn((float)p.w);
   const int64_t in_pitch = p.in_pitch, out_pitch = p.out_pitch;
@@ -522,9 +556,10 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
             continue;
           }
           f2 sv;
-          const f2 e = residual_pair<METHOD>(cq[0], cq[1], dq[0], dq[1], nu, nb, I, fa2, fb2, Lf2, sv);
+          const f2 e = residual_pair<METHOD>(cq[0], cq[1], dq[0], dq[1], nu, nb, I, fa2, fb2,
+                                             aux_operand<METHOD>(p, Lf2, nu), sv, y2);
           emin = fmin3(emin, fabsf(lo(e)), fabsf(hi(e)));
-          if (METHOD == M_NIBLACK) smin = fmin3(smin, lo(sv), hi(sv));
+          if (METHOD == M_NIBLACK || METHOD == M_KHURSHID) smin = fmin3(smin, lo(sv), hi(sv));
           e4[h2] = lo(e);
           e4[h2 + 1] = hi(e);
         }
@@ -546,7 +581,8 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
       // with the data-dependent bound at its smallest s~ (v4 refined_bound)
       uint32_t amb = 0u;
       if (emin < delta1) {
-        if (METHOD != M_NIBLACK || emin * 0.999999f < v4::refined_bound(p, smin)) amb = vmask;
+        if ((METHOD != M_NIBLACK && METHOD != M_KHURSHID) || emin * 0.999999f < v4::refined_bound(p, smin))
+          amb = vmask;
       }
       if (amb) {
         const uint32_t slot = atomicAdd(p.q_count, 1u);

@@ -48,8 +48,14 @@ int occ_v5(int method) {
   int n = 0;
   constexpr size_t smem = v5::smem_bytes();
   cudaError_t e;
-  static bool a0[64] = {}, a1[64] = {}, a2[64] = {};
-  if (method == M_SAUVOLA) {
+  static bool a0[64] = {}, a1[64] = {}, a2[64] = {}, a3[64] = {}, a4[64] = {};
+  if (method == M_KHURSHID) {
+    e = set_smem_attr_once(v5::k_mom5<W32, M_KHURSHID>, smem, a3);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, v5::k_mom5<W32, M_KHURSHID>, 32, smem);
+  } else if (method == M_PHANSALKAR) {
+    e = set_smem_attr_once(v5::k_mom5<W32, M_PHANSALKAR>, smem, a4);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, v5::k_mom5<W32, M_PHANSALKAR>, 32, smem);
+  } else if (method == M_SAUVOLA) {
     e = set_smem_attr_once(v5::k_mom5<W32, M_SAUVOLA>, smem, a0);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, v5::k_mom5<W32, M_SAUVOLA>, 32, smem);
   } else if (method == M_NIBLACK) {
@@ -67,6 +73,8 @@ cudaError_t launch_v5(const CUtensorMap& map, const MomParams& p, int64_t n_tile
   if (p.method == M_SAUVOLA) return launch_v5_m<W32, M_SAUVOLA>(map, p, n_tiles, st);
   if (p.method == M_NIBLACK) return launch_v5_m<W32, M_NIBLACK>(map, p, n_tiles, st);
   if (p.method == M_MAXS) return launch_v5_m<W32, M_MAXS>(map, p, n_tiles, st);
+  if (p.method == M_KHURSHID) return launch_v5_m<W32, M_KHURSHID>(map, p, n_tiles, st);
+  if (p.method == M_PHANSALKAR) return launch_v5_m<W32, M_PHANSALKAR>(map, p, n_tiles, st);
   return launch_v5_m<W32, M_WOLF>(map, p, n_tiles, st);
 }
 

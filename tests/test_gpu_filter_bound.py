@@ -28,6 +28,13 @@ LD = np.longdouble
 CHUNK = 4_000_000
 CHUNKS = 9                     # x 3 methods = 1.08e8 random tuples
 PARAMS = {"sauvola": (0.5, 128.0, 0.0), "niblack": (-0.2, 128.0, 0.0), "wolf": (0.5, 128.0, 17.0)}
+# the v5 rules (rule_params as abin_probe_filter takes them): Khurshid {k, N_mode, h w},
+# Phansalkar {k, R, p, q} (q >= 0; the configs' q = 10/255 and a steep q)
+RULES = {"khurshid0": ("khurshid", (-0.1, 0, 16383.0)), "khurshid0s": ("khurshid", (0.2, 0, 225.0)),
+         "khurshid1": ("khurshid", (-0.2, 1, 0.0)), "khurshidN1": ("khurshid", (0.3, 0, 1.0)),
+         "phansalkar": ("phansalkar", (0.25, 128.0, 3.0, 10.0 / 255.0)),
+         "phansalkar_steep": ("phansalkar", (-0.3, 64.0, -2.0, 0.5)),
+         "phansalkar_q0": ("phansalkar", (0.5, 128.0, 1.0, 0.0))}
 
 
 def t_exact(method, c, d, n, k, R, L):
@@ -36,6 +43,16 @@ def t_exact(method, c, d, n, k, R, L):
     nl = n.astype(LD)
     m = c.astype(LD) / nl
     s = np.sqrt(V.astype(LD) / (nl * nl))
+    if method in RULES:
+        rule, prm = RULES[method]
+        if rule == "khurshid":
+            # s^2 + m^2 (N - 1) / N = (N n d - c^2) / (N n^2), exact integers (N = h w or n)
+            N = n.astype(np.int64) if prm[1] else np.int64(prm[2])
+            U = N * n.astype(np.int64) * d.astype(np.int64) - c.astype(np.int64) ** 2
+            assert (U >= 0).all()
+            return m + LD(prm[0]) * np.sqrt(U.astype(LD) / (LD(1) * N * nl * nl))
+        kk, RR, pp, qq = (LD(x) for x in prm)
+        return m * (1 + pp * np.exp(-qq * m) + kk * (s / RR - 1))
     k, R, L = LD(k), LD(R), LD(L)
     if method == "sauvola":
         return m * (1 + k * (s / R - 1))
@@ -62,7 +79,7 @@ def random_tuples(rng, count):
 
 
 def adversarial_tuples(rng, method, count):
-    k, R, L = PARAMS[method]
+    k, R, L = PARAMS.get(method, (0.0, 1.0, 0.0))
     c, d, ncol, nrow, I = random_tuples(rng, count)
     n = ncol * nrow
     q = count // 6
@@ -88,23 +105,27 @@ def adversarial_tuples(rng, method, count):
 
 
 def run_probe(method, c, d, ncol, nrow, I):
-    k, R, L = PARAMS[method]
     dev = lambda a, dt: torch.from_numpy(a.astype(dt)).to(DEV)
-    e, sv, b = abin.probe_filter(method, dev(c, np.uint32), dev(d, np.uint32), dev(ncol, np.uint32),
-                                 dev(nrow, np.uint32), dev(I, np.uint8), k, R, L)
+    args = (dev(c, np.uint32), dev(d, np.uint32), dev(ncol, np.uint32), dev(nrow, np.uint32), dev(I, np.uint8))
+    if method in RULES:
+        rule, prm = RULES[method]
+        e, sv, b = abin.probe_filter(rule, *args, rule_params=prm)
+    else:
+        k, R, L = PARAMS[method]
+        e, sv, b = abin.probe_filter(method, *args, k, R, L)
     return e.cpu().numpy().astype(LD), sv.cpu().numpy().astype(np.float64), b
 
 
 def check(method, c, d, ncol, nrow, I):
-    k, R, L = PARAMS[method]
+    k, R, L = PARAMS.get(method, (0.0, 1.0, 0.0))
     e, sv, b = run_probe(method, c, d, ncol, nrow, I)
     e_star = I.astype(LD) - t_exact(method, c, d, ncol * nrow, k, R, L)
     err = np.abs(e - e_star).astype(np.float64)
     coarse = b[0]
     assert err.max() <= coarse, (method, err.max(), coarse)
     ratio = err.max() / coarse
-    if method == "niblack":
-        # the data-dependent bound the kernel applies to Niblack lanes
+    if method == "niblack" or method.startswith("khurshid"):
+        # the data-dependent bound the kernel applies to Niblack / Khurshid lanes
         with np.errstate(divide="ignore"):
             refined = b[1] + b[2] * np.minimum(b[4], b[3] / sv)
         assert (err <= refined).all(), (method, (err - refined).max())
@@ -130,3 +151,27 @@ def test_certified_bound_adversarial(method):
         worst = max(worst, check(method, *adversarial_tuples(rng, method, 1_000_000)))
     assert worst < 1.0
     print(f"{method}: 3e6 adversarial tuples, max |e~ - e*| / bound = {worst:.3g}")
+
+
+@pytest.mark.parametrize("method", sorted(RULES))
+def test_certified_bound_rules(method):
+    """Khurshid and Phansalkar on v5: the same claim |e~ - e*| <= bound for
+    the rule's own residual (moments5.cuh residual2, abin_api.cu
+    filter_consts_v5), e* from the exact integers in long double; 1.2e7
+    random + 3e6 adversarial tuples per parameter set (7 sets)."""
+    rng = np.random.default_rng(100 + sorted(RULES).index(method))
+    worst = 0.0
+    for _ in range(3):
+        worst = max(worst, check(method, *random_tuples(rng, CHUNK)))
+    for _ in range(3):
+        worst = max(worst, check(method, *adversarial_tuples(rng, method, 1_000_000)))
+    assert worst < 1.0
+    print(f"{method}: 1.5e7 tuples, max |e~ - e*| / bound = {worst:.3g}")
+
+
+def test_rule_parameters_outside_v5_are_refused():
+    z = torch.zeros(4, dtype=torch.uint32, device=DEV)
+    one = torch.ones(4, dtype=torch.uint32, device=DEV)
+    I = torch.zeros(4, dtype=torch.uint8, device=DEV)
+    with pytest.raises(abin.AbinError):   # q < 0: e^(-q m) unbounded -> exact path only
+        abin.probe_filter("phansalkar", z, z, one, one, I, rule_params=(0.25, 128.0, 3.0, -0.1))
