@@ -30,6 +30,7 @@ METHODS = {"sauvola": SAUVOLA, "niblack": NIBLACK, "wolf": WOLF, "quantile": QUA
 MASK_U8, MASK_BITS = 0, 1
 FORCE_U64_SQ, FORCE_FP64, HOST_IO, COUNT_STAGES = 1, 2, 4, 8
 V4_INTERNAL = 1 << 27  # internal test hook: the v4 warp-CTA kernel instead of v5 (A/B parity)
+Q2_INTERNAL = 1 << 26  # internal test hook: the round-1 quantile kernels instead of v5 (A/B parity)
 V3_INTERNAL = 1 << 29  # internal test hook: the 4-warp-CTA kernel instead of the warp-CTA kernel
 NO_TMA_INTERNAL = 1 << 30  # internal test hook: the generic row loader (no TMA, no re-pitched copy)
 OK, EINVAL, EALIAS, ERANGE, ECUDA, ENOMEM = 0, 1, 2, 3, 4, 5

@@ -1,7 +1,8 @@
 """Build libabin.so (the CUDA kernels + C ABI) in-tree for sm_100a.
 
 The kernel template instantiations are spread over several translation units
-(csrc/moments_part.cu x 8, csrc/wide_part.cu x 2, csrc/abin_api.cu) that nvcc
+(csrc/moments_part.cu x 8, csrc/wide_part.cu x 2, csrc/quant5_part.cu x 4,
+csrc/abin_api.cu) that nvcc
 compiles in parallel into build/*.o; they are then linked into one shared
 library.
 """
@@ -31,6 +32,7 @@ def units():
     u = [("abin_api.o", "abin_api.cu", [])]
     u += [(f"moments_part{k}.o", "moments_part.cu", [f"-DABIN_PART={k}"]) for k in range(N_PARTS)]
     u += [(f"wide_part{d}.o", "wide_part.cu", [f"-DABIN_WIDE_D64={d}"]) for d in (0, 1)]
+    u += [(f"quant5_part{k}.o", "quant5_part.cu", [f"-DABIN_Q5_PART={k}"]) for k in range(4)]
     return u
 
 

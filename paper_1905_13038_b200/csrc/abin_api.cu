@@ -81,6 +81,7 @@ constexpr uint32_t ABIN_NO_TMA_INTERNAL = 1u << 30;
 constexpr uint32_t ABIN_V3_INTERNAL = 1u << 29;
 constexpr uint32_t ABIN_WIDE_INTERNAL = 1u << 28;  // test hook: the CTA-wide kernel for any window
 constexpr uint32_t ABIN_V4_INTERNAL = 1u << 27;    // test hook: the v4 warp-CTA kernel instead of v5
+constexpr uint32_t ABIN_Q2_INTERNAL = 1u << 26;    // test hook: the round-1 quantile kernels instead of v5
 constexpr int64_t kMaxDim = (int64_t)1 << 30;
 constexpr int kQuantNT = 128;  // threads of the single-column quantile kernel (its staging bounds w)
 
@@ -770,11 +771,116 @@ int check_params(int32_t method, double p0, double p1) {
 }
 
 
+int launch_q5_any(int wr, const q5::Q5Params& p, int64_t n, cudaStream_t st, int* occ) {
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (wr >> 2) {
+    case 0: e = launch_q5_part0(wr, p, n, st, occ); break;
+    case 1: e = launch_q5_part1(wr, p, n, st, occ); break;
+    case 2: e = launch_q5_part2(wr, p, n, st, occ); break;
+    case 3: e = launch_q5_part3(wr, p, n, st, occ); break;
+  }
+  return e == cudaSuccess ? ABIN_OK : cuda_fail(e);
+}
+
+// The v5 quantile kernel (quantile5.cuh) for the mask of method 3 where it
+// applies: h <= 255, w <= 127 (vector row loads / mask stores where the
+// pointers and pitches are aligned).  Returns -1 (nothing launched) otherwise.
+int run_quant5(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64_t W, int64_t in_pitch, uint8_t* out,
+               int64_t out_pitch, int64_t out_page_stride, int32_t fmt, const Window& win, double q, int64_t row0,
+               int64_t H_out, int64_t H_global, int64_t buf_rows, int64_t buf_row0, cudaStream_t st,
+               uint64_t* counters) {
+  if (win.w > q5::kMaxW || win.h > q5::kMaxH) return -1;
+  q5::Q5Params p;
+  memset(&p, 0, sizeof(p));
+  // vector loads / stores where the rows allow (else byte-wise, same results)
+  const uintptr_t ia = reinterpret_cast<uintptr_t>(in), oa = reinterpret_cast<uintptr_t>(out);
+  p.in_vec = !((ia & 15) || (in_pitch & 15) || (n_pages > 1 && (in_page_stride & 15)));
+  const int64_t oal = fmt == ABIN_MASK_U8 ? 16 : 2;
+  p.out_vec = !((int64_t)(oa % oal) || out_pitch % oal || (n_pages > 1 && out_page_stride % oal));
+  p.in = in; p.in_page_stride = in_page_stride; p.in_pitch = in_pitch; p.W = W;
+  p.buf_row0 = buf_row0; p.buf_rows = buf_rows; p.row0 = row0; p.H_out = H_out; p.H_global = H_global;
+  p.out = out; p.out_pitch = out_pitch; p.out_page_stride = out_page_stride; p.fmt = fmt;
+  p.h = win.h; p.w = win.w; p.l = win.l; p.r = win.r; p.o = win.o; p.u = win.u;
+  p.q = q;
+  p.KH = (win.w + 15) / 16;
+  p.mq = win.w / 16;
+  p.Tw = 16 * (32 - p.KH);
+  p.n_strips = (int32_t)((W + p.Tw - 1) / p.Tw);
+  // windows per tile: the median-like quantiles of document pages sit in the
+  // background's level range (one window); the low ones in either the
+  // strokes' or the background's (three windows placed at q/2, q, 2q of the
+  // tile sample).  ABIN_Q5_NW overrides (experiments).
+  int nw = q >= 0.2 ? 1 : 3;
+  if (const char* e = getenv("ABIN_Q5_NW")) nw = std::max(1, std::min(q5::kMaxNW, atoi(e)));
+  p.nw = nw;
+  const float qf = (float)q;
+  if (nw == 1) { p.qf[0] = qf; }
+  else if (nw == 2) { p.qf[0] = 0.5f * qf; p.qf[1] = std::min(1.0f, 2.0f * qf); }
+  else { p.qf[0] = 0.5f * qf; p.qf[1] = qf; p.qf[2] = std::min(1.0f, 2.0f * qf); }
+  p.force_L = -1;
+  if (const char* e = getenv("ABIN_Q5_FORCE_L")) p.force_L = std::max(0, std::min(240, atoi(e)));  // tests
+  const int wr = win.w % 16;
+  int occ = 0;
+  int rc = launch_q5_any(wr, p, 0, st, &occ);
+  if (rc) return rc;
+  {
+    // bands: minimise waves x tile cost, a tile costing its B output rows plus
+    // the h warm-up rows (column adds only: about a fifth of a row each) and
+    // its set-up (sample histogram, tables: about four rows)
+    const int64_t cols = (int64_t)p.n_strips * n_pages, slots = (int64_t)num_sms() * std::max(1, occ);
+    static const char* wu_env = getenv("ABIN_Q5_WU");  // experiments: warm-up row weight
+    const double wu = wu_env ? atof(wu_env) : 0.2;
+    double best = 1e300;
+    int64_t bestB = H_out;
+    for (int64_t nb = 1; nb <= std::max<int64_t>(1, H_out / 4); ++nb) {
+      const int64_t Bc = (H_out + nb - 1) / nb;
+      const int64_t waves = (cols * ((H_out + Bc - 1) / Bc) + slots - 1) / slots;
+      const double cost = (double)waves * ((double)Bc + wu * win.h + 4.0);
+      if (cost < best * 0.999) { best = cost; bestB = Bc; }
+      if (cols * nb > 64 * slots) break;
+    }
+    if (const char* nb = getenv("ABIN_Q5_BANDS")) {  // experiments: force the band count
+      const int64_t want = std::max<int64_t>(1, std::min<int64_t>(atoll(nb), H_out));
+      bestB = (H_out + want - 1) / want;
+    }
+    p.B = (int32_t)bestB;
+    p.n_bands = (int32_t)((H_out + bestB - 1) / bestB);
+  }
+  // the exact queue: 16 bytes per undecided pixel; a full queue is decided inline
+  const int64_t px = n_pages * H_out * W;
+  uint32_t cap = (uint32_t)std::min<int64_t>(px, 1 << 20);
+  if (const char* e = getenv("ABIN_Q5_QCAP")) cap = (uint32_t)std::max<long long>(1, std::min<long long>(atoll(e), cap));
+  uint4* queue = nullptr;
+  CK(cudaMallocAsync(&queue, (size_t)cap * 16 + 16, st));
+  uint32_t* qcount = reinterpret_cast<uint32_t*>(queue + cap);
+  CK(cudaMemsetAsync(qcount, 0, 4, st));
+  p.fq = queue; p.fq_count = qcount; p.fq_cap = cap;
+  p.counters = reinterpret_cast<unsigned long long*>(counters);
+  const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * n_pages;
+  if (getenv("ABIN_DEBUG"))
+    fprintf(stderr, "q5: w %d h %d nw %d strips %d bands %d B %d occ %d tiles %lld\n", win.w, win.h, nw, p.n_strips,
+            p.n_bands, p.B, occ, (long long)n_tiles);
+  rc = launch_q5_any(wr, p, n_tiles, st, nullptr);
+  if (rc == ABIN_OK) {
+    q5::k_q5fix<<<num_sms() * 2, 256, 0, st>>>(p);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) rc = cuda_fail(e);
+  }
+  const cudaError_t f = cudaFreeAsync(queue, st);
+  if (rc == ABIN_OK && f != cudaSuccess) return cuda_fail(f);
+  return rc;
+}
+
 int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64_t /*H_held*/, int64_t W,
                  int64_t in_pitch, uint8_t* out, int64_t out_pitch, int64_t out_page_stride, int32_t fmt, int32_t h,
                  int32_t w, double q, int64_t row0, int64_t H_out, int64_t H_global, int64_t buf_rows,
-                 int64_t buf_row0, cudaStream_t st, double* Q_out) {
+                 int64_t buf_row0, cudaStream_t st, double* Q_out, uint32_t flags, uint64_t* counters) {
   const Window win = effective_window(h, w, H_global, W);
+  if (method == ABIN_QUANTILE && !Q_out && !(flags & ABIN_Q2_INTERNAL)) {
+    const int rc = run_quant5(in, in_page_stride, n_pages, W, in_pitch, out, out_pitch, out_page_stride, fmt, win, q,
+                              row0, H_out, H_global, buf_rows, buf_row0, st, counters);
+    if (rc >= 0) return rc;
+  }
   constexpr int NT_ = kQuantNT;
   if ((int64_t)win.h * win.w > 65535) return ABIN_ERANGE;  // u16 bins
   if (NT_ + win.w - 1 > 4 * NT_) return ABIN_ERANGE;  // a thread stages at most 4 elements of a row
@@ -899,7 +1005,7 @@ int run_moments(const MomCall& c);
 int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64_t H_held, int64_t W,
                  int64_t in_pitch, uint8_t* out, int64_t out_pitch, int64_t out_page_stride, int32_t fmt, int32_t h,
                  int32_t w, double q, int64_t row0, int64_t H_out, int64_t H_global, int64_t buf_rows,
-                 int64_t buf_row0, cudaStream_t st, double* Q_out);
+                 int64_t buf_row0, cudaStream_t st, double* Q_out, uint32_t flags, uint64_t* counters);
 
 // Host <-> device copies of `rows` rows of `width` bytes.  Only the caller's
 // `width` bytes per row are read or written (the padding of a row and the
@@ -987,7 +1093,7 @@ int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8
         CK(copy_rows_h2d(din, dpitch, src, in_pitch, W, held, s));
         if (method == ABIN_QUANTILE || method == ABIN_BERNSEN) {
           rc = run_quantile(method, din, 0, 1, held, W, dpitch, dout, dopitch, 0, fmt, h, w, p0, r0, r1 - r0, H, held,
-                            r0 - top, s, nullptr);
+                            r0 - top, s, nullptr, flags, counters);
         } else {
           MomCall m;
           memset(&m, 0, sizeof(m));
@@ -1014,7 +1120,8 @@ int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8
       for (int64_t q = 0; q < np; ++q) CK(copy_rows_h2d(din + q * dpage, dpitch, in + (c0 + q) * in_page_stride, in_pitch, W, H, s));
     }
     if (method == ABIN_QUANTILE || method == ABIN_BERNSEN) {
-      rc = run_quantile(method, din, dpage, np, H, W, dpitch, dout, dopitch, dopage, fmt, h, w, p0, 0, H, H, H, 0, s, nullptr);
+      rc = run_quantile(method, din, dpage, np, H, W, dpitch, dout, dopitch, dopage, fmt, h, w, p0, 0, H, H, H, 0, s, nullptr,
+                        flags, counters);
     } else {
       MomCall m;
       memset(&m, 0, sizeof(m));
@@ -1068,7 +1175,7 @@ int abin_binarize_batched(int32_t method, const uint8_t* in, int64_t in_page_str
                        mask_format, h, w, param0, param1, L_override, flags, counters, st);
   if (method == ABIN_QUANTILE || method == ABIN_BERNSEN)
     return run_quantile(method, in, in_page_stride, n_pages, H, W, in_pitch, out, out_pitch, out_page_stride, mask_format, h,
-                        w, param0, 0, H, H, H, 0, st, nullptr);
+                        w, param0, 0, H, H, H, 0, st, nullptr, flags, counters);
   MomCall c;
   memset(&c, 0, sizeof(c));
   c.method = method;
@@ -1214,7 +1321,7 @@ int abin_binarize_band(int32_t method, const uint8_t* in, int64_t H_band, int64_
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (method == ABIN_QUANTILE || method == ABIN_BERNSEN)
     return run_quantile(method, in, 0, 1, held, W, in_pitch, out, out_pitch, 0, mask_format, h, w, param0, row0, H_band,
-                        H_global, held, row0 - halo_top, st, nullptr);
+                        H_global, held, row0 - halo_top, st, nullptr, flags, counters);
   MomCall c;
   memset(&c, 0, sizeof(c));
   c.method = method;
@@ -1268,7 +1375,8 @@ int abin_stats(int32_t method, const uint8_t* in, int64_t H, int64_t W, int64_t 
   uint8_t* scratch = nullptr;  // the mask also goes to a throwaway U8 buffer
   CK(cudaMallocAsync(&scratch, (size_t)(H * W), st));
   if (method == ABIN_QUANTILE || method == ABIN_BERNSEN) {
-    rc = run_quantile(method, in, 0, 1, H, W, in_pitch, scratch, W, 0, ABIN_MASK_U8, h, w, param0, 0, H, H, H, 0, st, t_out);
+    rc = run_quantile(method, in, 0, 1, H, W, in_pitch, scratch, W, 0, ABIN_MASK_U8, h, w, param0, 0, H, H, H, 0, st, t_out,
+                      0, nullptr);
   } else {
     MomCall c;
     memset(&c, 0, sizeof(c));

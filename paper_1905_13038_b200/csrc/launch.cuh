@@ -10,6 +10,7 @@
 #include "moments_wide.cuh"
 #include "moments4.cuh"
 #include "moments5.cuh"
+#include "quantile5.cuh"
 
 namespace abin {
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize, carveout) once per device
@@ -43,6 +44,11 @@ cudaError_t launch_wide(bool d64, bool stats, int nt, int ph, const CUtensorMap&
   int occupancy_v5_part##k(int w32, int method);
 ABIN_DECL_PART(0) ABIN_DECL_PART(1) ABIN_DECL_PART(2) ABIN_DECL_PART(3)
 ABIN_DECL_PART(4) ABIN_DECL_PART(5) ABIN_DECL_PART(6) ABIN_DECL_PART(7)
+// v5 quantile kernel (quantile5.cuh), split by w mod 16 (quant5_part.cu); occ != nullptr: occupancy query
+cudaError_t launch_q5_part0(int wr, const q5::Q5Params& p, int64_t n, cudaStream_t st, int* occ);
+cudaError_t launch_q5_part1(int wr, const q5::Q5Params& p, int64_t n, cudaStream_t st, int* occ);
+cudaError_t launch_q5_part2(int wr, const q5::Q5Params& p, int64_t n, cudaStream_t st, int* occ);
+cudaError_t launch_q5_part3(int wr, const q5::Q5Params& p, int64_t n, cudaStream_t st, int* occ);
 cudaError_t launch_wide_d64(bool d64, bool stats, int nt, int ph, const CUtensorMap& map, const wide::MomParams& p,
                             int64_t n_tiles, cudaStream_t st);
 cudaError_t launch_wide_d32(bool d64, bool stats, int nt, int ph, const CUtensorMap& map, const wide::MomParams& p,

@@ -240,22 +240,27 @@ def test_quantile_small(q):
         assert np.array_equal(s["t"].cpu().numpy(), Qref.astype(np.float64))
 
 
-@pytest.mark.parametrize("single", [False, True])
+@pytest.mark.parametrize("kernel", ["v5", "pair", "single"])
 @pytest.mark.parametrize("hw", [(3, 3), (12, 7), (51, 51), (125, 40), (126, 40), (30, 128), (30, 129)])
-def test_quantile_both_kernels(monkeypatch, single, hw):
-    """The paired-column kernel (k_quantile2, default where its packing
-    allows: h <= 125, w <= 128) and the single-column kernel (forced with
-    ABIN_QUANTILE_SINGLE, and taken beyond those limits) against the oracle:
-    odd widths (a last thread with one active column), bit masks, a page batch
-    and the Q statistics; windows on both sides of the limits."""
-    if single:
+def test_quantile_all_kernels(monkeypatch, kernel, hw):
+    """The v5 kernel (quantile5.cuh, default for masks with h <= 255,
+    w <= 127), the paired-column kernel (k_quantile2: forced with the
+    Q2_INTERNAL hook where its packing allows, h <= 125, w <= 128) and the
+    single-column kernel (ABIN_QUANTILE_SINGLE, and beyond those limits)
+    against the oracle: odd widths (a last thread with one active column), bit
+    masks, a page batch and the Q statistics; windows on both sides of the
+    limits."""
+    flags = 0 if kernel == "v5" else abin.Q2_INTERNAL
+    if kernel == "single":
         monkeypatch.setenv("ABIN_QUANTILE_SINGLE", "1")
     h, w = hw
     pages = _quantile_pages()
-    x = torch.from_numpy(pages).to(DEV)
+    buf = torch.zeros((2, 120, 272), dtype=torch.uint8, device=DEV)  # 16-byte aligned rows (v5)
+    buf[:, :, :261] = torch.from_numpy(pages).to(DEV)
+    x = buf[:, :, :261]
     for q in (0.5, 0.1):
-        mb = ab.binarize_batched("quantile", x, h, w, q).cpu().numpy()
-        bits = ab.binarize_batched("quantile", x, h, w, q, packed=True).cpu().numpy()
+        mb = ab.binarize_batched("quantile", x, h, w, q, flags=flags).cpu().numpy()
+        bits = ab.binarize_batched("quantile", x, h, w, q, packed=True, flags=flags).cpu().numpy()
         for p in range(2):
             mref, Qref = _quantile_ref(p, h, w, q)
             assert np.array_equal(mb[p], mref), (hw, q, p)
