@@ -165,6 +165,19 @@ __device__ __forceinline__ void q5_body(const Q5Params& p, uint8_t* sm, int stri
   const int64_t jl = J0 + 16 * (lane - p.KH);          // this lane's first output column
 
   // one 16-byte staged chunk of row g: columns [A + 16 q, +16), zero outside
+  // chunk qc of a row given by its pointer (nullptr: absent row)
+  auto load_rchunk = [&](const uint8_t* row, int qc) -> uint4 {
+    const uint4 v = make_uint4(~0u, ~0u, ~0u, ~0u);  // absent: 255
+    if (row == nullptr) return v;
+    const int64_t cc = A + 16 * qc;
+    if (!EDGE) return p.in_vec ? __ldg(reinterpret_cast<const uint4*>(row + cc)) : load16_bytes(row, cc, p.W);
+    if (cc + 16 <= 0 || cc >= p.W) return v;
+    if (p.in_vec && cc >= 0 && cc + 16 <= p.W) return __ldg(reinterpret_cast<const uint4*>(row + cc));
+    return load16_bytes(row, cc, p.W);
+  };
+  auto row_at = [&](int64_t g) -> const uint8_t* {
+    return (g < lo_row || g >= hi_row) ? nullptr : img + (g - p.buf_row0) * p.in_pitch;
+  };
   auto load_chunk = [&](int64_t g, int qc) -> uint4 {
     const uint4 v = make_uint4(~0u, ~0u, ~0u, ~0u);  // absent: 255
     if (g < lo_row || g >= hi_row) return v;
@@ -405,10 +418,12 @@ __device__ __forceinline__ void q5_body(const Q5Params& p, uint8_t* sm, int stri
   uint8_t* obase = p.out + (int64_t)page * p.out_page_stride;
   uint4 nin, nout, nin32, nout32, nctr;
   if (nrows > 0) {
-    nin = load_chunk(y0 + p.u, lane);
-    nout = load_chunk(y0 - p.o, lane);
-    nin32 = lane == 0 ? load_chunk(y0 + p.u, 32) : make_uint4(0u, 0u, 0u, 0u);
-    nout32 = lane == 0 ? load_chunk(y0 - p.o, 32) : make_uint4(0u, 0u, 0u, 0u);
+    const uint8_t* ri = row_at(y0 + p.u);
+    const uint8_t* ro = row_at(y0 - p.o);
+    nin = load_rchunk(ri, lane);
+    nout = load_rchunk(ro, lane);
+    nin32 = lane == 0 ? load_rchunk(ri, 32) : make_uint4(0u, 0u, 0u, 0u);
+    nout32 = lane == 0 ? load_rchunk(ro, 32) : make_uint4(0u, 0u, 0u, 0u);
     nctr = load_centre(y0);
   }
   for (int qq = 0; qq < nrows; ++qq) {
@@ -422,11 +437,13 @@ __device__ __forceinline__ void q5_body(const Q5Params& p, uint8_t* sm, int stri
     const uint4 ctr = nctr;
     __syncwarp();
     if (qq + 1 < nrows) {
-      nin = load_chunk(i + 1 + p.u, lane);
-      nout = load_chunk(i + 1 - p.o, lane);
+      const uint8_t* ri = row_at(i + 1 + p.u);
+      const uint8_t* ro = row_at(i + 1 - p.o);
+      nin = load_rchunk(ri, lane);
+      nout = load_rchunk(ro, lane);
       if (lane == 0) {
-        nin32 = load_chunk(i + 1 + p.u, 32);
-        nout32 = load_chunk(i + 1 - p.o, 32);
+        nin32 = load_rchunk(ri, 32);
+        nout32 = load_rchunk(ro, 32);
       }
       nctr = load_centre(i + 1);
     }
@@ -483,7 +500,7 @@ __device__ __forceinline__ void q5_body(const Q5Params& p, uint8_t* sm, int stri
         const int64_t ncol = min(j + p.r, p.W - 1) - max(j - p.l, (int64_t)-1);
         dK = (uint32_t)(rho_row - rank_of(p.q, ncol * nrow)) * 0x10001u;
       }
-      uint32_t known = 0u, mk = 0u;
+      bool mk = false, unk = true;
 #pragma unroll
       for (int k = 0; k < NW; ++k) {
         const uint32_t cbk = colb_a + k * (16 * 512);
@@ -508,12 +525,18 @@ __device__ __forceinline__ void q5_body(const Q5Params& p, uint8_t* sm, int stri
         // I' = [I - L >= 16 - fge]; undecided: below the window with every
         // level >= rho, or above it with none
         const int f = It - L[k];
-        const uint32_t kn = ((f < 0 && fge == 16) || (f > 15 && fge == 0)) ? 0u : 1u;
-        mk |= kn & ((f + fge >= 16) ? 1u : 0u);
-        known |= kn;
+        const bool u_k = (unsigned)f > 15u && fge == (f < 0 ? 16 : 0);
+        const bool m_k = f + fge >= 16;
+        if (NW == 1) {
+          mk = m_k;
+          unk = u_k;
+        } else {
+          mk = mk || (!u_k && m_k);
+          unk = unk && u_k;
+        }
       }
-      mbits |= mk << t;
-      ubits |= (known ^ 1u) << t;
+      if (mk) mbits |= 1u << t;
+      if (unk) ubits |= 1u << t;
     }
     }
     // outputs of this lane: columns jl .. jl + 15 (inside the image)
@@ -525,7 +548,7 @@ __device__ __forceinline__ void q5_body(const Q5Params& p, uint8_t* sm, int stri
         if (jl + t >= 0 && jl + t < p.W) vmask |= 1u << t;
     }
     ubits &= vmask;
-    mbits &= vmask;
+    mbits &= vmask & ~ubits;  // undecided pixels: 0 until the exact decision
     if (__any_sync(0xffffffffu, ubits != 0u)) {
       // undecided pixels: exact queue (warp-aggregated slots)
       const uint32_t cnt = __popc(ubits);
