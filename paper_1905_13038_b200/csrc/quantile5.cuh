@@ -44,6 +44,9 @@ constexpr int kG = 16;         // columns per lane
 constexpr int kMaxW = 127;     // KH <= 8
 constexpr int kMaxH = 127;     // byte column counts; |C_in - C_out| <= 127 for the biased difference
 constexpr int kMaxNW = 3;
+#ifndef ABIN_Q5_MINB
+#define ABIN_Q5_MINB 12  // resident warps / SM the registers are sized for (A/B: 14, 16 spill)
+#endif
 constexpr int kLut = 256;      // thermometer entries (absent pixels staged as 255: entry 0)
 
 struct Q5Params {
@@ -613,7 +616,7 @@ __device__ __forceinline__ void q5_body(const Q5Params& p, uint8_t* sm, int stri
 }
 
 template <int WR, int NW>
-__global__ void __launch_bounds__(32, 12) k_quant5(const __grid_constant__ Q5Params p) {
+__global__ void __launch_bounds__(32, ABIN_Q5_MINB) k_quant5(const __grid_constant__ Q5Params p) {
   extern __shared__ __align__(16) uint8_t q5sm[];
   int64_t tile = blockIdx.x;
   const int strip = (int)(tile % p.n_strips);
