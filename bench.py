@@ -355,10 +355,14 @@ def ours_main(args):
                     ab.sauvola(x[0], h, w, k, R, packed=packed, out=o[0], flags=flags, counters=counters)
             else:
                 ab.binarize_batched(method, x, h, w, k, R, packed=packed, out=o, flags=flags, counters=counters)
-        # quantile: one kernel; moments: the v5 kernel + exact fixup (+ the v3
+        # quantile: the v5 kernel + its exact queue (q >= 0.2; the round-1
+        # kernel alone below); moments: the v5 kernel + exact fixup (+ the v3
         # overflow follow-up when the queue could overflow: its CTAs exit at
         # once unless it did); Wolf adds the fill + global-minimum pre-pass
-        launches_per_step = 0 if P == 0 else (1 if method == "quantile" else (5 if method == "wolf" else 3))
+        if method == "quantile":
+            launches_per_step = 0 if P == 0 else (2 if k >= 0.2 else 1)
+        else:
+            launches_per_step = 0 if P == 0 else (5 if method == "wolf" else 3)
         if sweep:
             launches_per_step = 3 * len(SWEEP)
         l2_note = (f"inputs {step_bytes / 1e9:.2f} GB per rank per step > L2: no flush needed" if n_copies == 1 else

@@ -13,7 +13,7 @@ ncu -i /tmp/${tag}_c3.ncu-rep --page raw --csv > gpurun_out/prof/${tag}_c3_raw.c
 ncu -i /tmp/${tag}_c3.ncu-rep --page details --csv > gpurun_out/prof/${tag}_c3_details.csv 2>/dev/null
 ncu -i /tmp/${tag}_c3.ncu-rep --page source --csv --print-source sass 2>/dev/null | gzip > gpurun_out/prof/${tag}_c3_sass.csv.gz
 python bench.py --config 5 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1 && \
-ncu -f --set full --clock-control none --import-source on -k regex:k_quantile -c 1 -o /tmp/${tag}_c5 \
+ncu -f --set full --clock-control none --import-source on -k regex:k_quant -c 1 -o /tmp/${tag}_c5 \
     python bench.py --config 5 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/prof/ncu_c5.log 2>&1
 ncu -i /tmp/${tag}_c5.ncu-rep --page raw --csv > gpurun_out/prof/${tag}_c5_raw.csv 2>/dev/null
 ncu -i /tmp/${tag}_c5.ncu-rep --page details --csv > gpurun_out/prof/${tag}_c5_details.csv 2>/dev/null
