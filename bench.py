@@ -529,7 +529,9 @@ def ours_main(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: 50 for configs 3/4/5b, more for the short single-page steps so "
+                         "the timed region spans tens of ms: 1000 for config 1, 100 for 2, 200 for 5)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=cfg_key, default=3, choices=list(CONFIGS))
@@ -537,6 +539,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = {1: 1000, 2: 100, 5: 200}.get(args.config, 50) if args.impl == "ours" else 50
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":

@@ -486,6 +486,8 @@ static void keep_pool_warm() {
   done[dev] = true;
 }
 
+int launch_fixup(const MomParams& q, int w, cudaStream_t st);
+
 int run_moments(const MomCall& c) {
   keep_pool_warm();
   const Window win = effective_window(c.h, c.w, c.H_global, c.W);
@@ -677,28 +679,14 @@ int run_moments(const MomCall& c) {
         rc = launch_v5_any(w32, map4, q, n_tiles, c.stream);
         q.maxs_pass = 1;
         if (rc == ABIN_OK) rc = launch_v5_any(w32, map4, q, n_tiles, c.stream);
-        if (rc == ABIN_OK) {
-          const size_t fsm = fixup_smem_bytes(win.w);
-          if (fsm > 48 * 1024) CK(cudaFuncSetAttribute(k_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-          int per_sm = 0;
-          CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fixup, kFixNT, fsm));
-          k_fixup<<<num_sms() * std::max(1, per_sm), kFixNT, fsm, c.stream>>>(q);
-          CK(cudaGetLastError());
-        }
+        if (rc == ABIN_OK) rc = launch_fixup(q, win.w, c.stream);
         cudaError_t e1 = cudaFreeAsync(vmax, c.stream), e2 = cudaFreeAsync(queue, c.stream);
         if (rc == ABIN_OK && e1 != cudaSuccess) return cuda_fail(e1);
         if (rc == ABIN_OK && e2 != cudaSuccess) return cuda_fail(e2);
         return rc;
       }
       rc = use_v5 ? launch_v5_any(w32, map4, q, n_tiles, c.stream) : launch_v4_any(w32, d64, map4, q, n_tiles, c.stream);
-      if (rc == ABIN_OK) {
-        const size_t fsm = fixup_smem_bytes(win.w);
-        if (fsm > 48 * 1024) CK(cudaFuncSetAttribute(k_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-        int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fixup, kFixNT, fsm));
-        k_fixup<<<num_sms() * std::max(1, per_sm), kFixNT, fsm, c.stream>>>(q);
-        CK(cudaGetLastError());
-      }
+      if (rc == ABIN_OK) rc = launch_fixup(q, win.w, c.stream);
       if (rc == ABIN_OK && may_overflow) {
         // overflow (pathological inputs only): the v3 kernel redoes the call
         // exactly; its CTAs return at once when the queue held everything
@@ -770,6 +758,56 @@ int check_params(int32_t method, double p0, double p1) {
   return ABIN_OK;
 }
 
+
+// k_fixup after the moments kernel on the same stream.  Its CTAs only read
+// the queue count and exit when the fp32 filter decided every pixel, so the
+// launch itself is the cost for most calls: occupancy is cached per device
+// and window, and the launch is programmatic (PDL): the grid is scheduled as
+// the moments kernel drains and waits in griddepcontrol.wait for its results.
+int launch_fixup(const MomParams& q, int w, cudaStream_t st) {
+  const size_t fsm = fixup_smem_bytes(w);
+  static std::mutex mu;
+  static int cache_w[64][8];
+  static int cache_n[64][8];
+  static bool inited[64] = {};
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return ABIN_EINVAL;
+  int per_sm = -1;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!inited[dev]) {
+      for (int z = 0; z < 8; ++z) cache_w[dev][z] = -1;
+      inited[dev] = true;
+    }
+    for (int z = 0; z < 8; ++z)
+      if (cache_w[dev][z] == w) per_sm = cache_n[dev][z];
+  }
+  if (per_sm < 0) {
+    if (fsm > 48 * 1024) CK(cudaFuncSetAttribute(k_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fixup, kFixNT, fsm));
+    std::lock_guard<std::mutex> lock(mu);
+    for (int z = 7; z > 0; --z) { cache_w[dev][z] = cache_w[dev][z - 1]; cache_n[dev][z] = cache_n[dev][z - 1]; }
+    cache_w[dev][0] = w;
+    cache_n[dev][0] = per_sm;
+  }
+  const unsigned grid = (unsigned)(num_sms() * std::max(1, per_sm));
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kFixNT);
+    cfg.dynamicSmemBytes = fsm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_fixup, q));
+  }
+  CK(cudaGetLastError());
+  return ABIN_OK;
+}
 
 int launch_q5_any(int wr, const q5::Q5Params& p, int64_t n, cudaStream_t st, int* occ) {
   cudaError_t e = cudaErrorInvalidValue;
@@ -862,8 +900,17 @@ int run_quant5(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64
             p.n_bands, p.B, occ, (long long)n_tiles);
   rc = launch_q5_any(wr, p, n_tiles, st, nullptr);
   if (rc == ABIN_OK) {
-    q5::k_q5fix<<<num_sms() * 2, 256, 0, st>>>(p);
-    const cudaError_t e = cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};  // programmatic launch (PDL), as launch_fixup
+    cfg.gridDim = dim3((unsigned)(num_sms() * 2));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, q5::k_q5fix, p);
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) rc = cuda_fail(e);
   }
   const cudaError_t f = cudaFreeAsync(queue, st);

@@ -58,6 +58,8 @@ static __global__ void __launch_bounds__(kFixNT, 4) k_fixup(const MomParams p) {
   uint32_t* my = reinterpret_cast<uint32_t*>(wbase) + lane * rstride;  // this lane's staged row
   unsigned long long* sd = reinterpret_cast<unsigned long long*>(wbase + fixup_stage_bytes(p.w));  // [32][16]
   uint32_t* sc = reinterpret_cast<uint32_t*>(sd + 32 * 16);                                          // [32][16]
+  // programmatic launch (PDL): wait for the moments kernel's queue and mask
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t count = *p.q_count;
   const uint32_t nq = count > p.q_cap ? 0u : count;
   unsigned long long near = 0, fb64 = 0, st2 = 0;

@@ -58,6 +58,9 @@ constexpr int kSpan = 16 * kChunks;       // staged bytes per row
 #ifndef ABIN_V5_KR
 #define ABIN_V5_KR 3
 #endif
+#ifndef ABIN_V5_L2
+#define ABIN_V5_L2 0  // L2 policy experiments: 1 mask stores evict_first, 2 entering rows evict_normal, 4 leaving rows evict_normal
+#endif
 constexpr int kR = ABIN_V5_KR;            // rows per ring stage and stream
 constexpr int kNS = 2;                    // ring stages
 constexpr int kRowsBytes = (kR * kSpan + 127) / 128 * 128;
@@ -260,7 +263,8 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
   auto issue = [&](int s) {  // lane 0 only
     const int slot = s % kNS;
     uint8_t* st = ring + slot * kStageBytes;
-    const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
+    const uint64_t keep = (ABIN_V5_L2 & 2) ? policy_evict_normal() : policy_evict_last();
+    const uint64_t drop = (ABIN_V5_L2 & 4) ? policy_evict_normal() : policy_evict_first();
     mbar_arrive_expect_tx(&full[slot], 2 * kR * kSpan);
     if (s < WS) {  // warm-up rows y0-o+2kR s .. +2kR-1 into both halves of the slot
       const int32_t yw = (int32_t)(y0 - p.o + (int64_t)s * 2 * kR - p.buf_row0);
@@ -591,7 +595,8 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
       // ---- store the mask: outputs j0 .. j0+15
       if (store_mode != 0u) {
         if (store_mode == 1u) {
-          __stcs(reinterpret_cast<uint4*>(optr), make_uint4(wv[0], wv[1], wv[2], wv[3]));  // streaming
+          if (ABIN_V5_L2 & 1) st_global_hint(optr, make_uint4(wv[0], wv[1], wv[2], wv[3]), policy_evict_first());
+          else __stcs(reinterpret_cast<uint4*>(optr), make_uint4(wv[0], wv[1], wv[2], wv[3]));  // streaming
         } else if (store_mode == 2u) {
 #pragma unroll
           for (int t = 0; t < kG; ++t)
@@ -621,6 +626,8 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
 // One launch for all strips: the border strips get the low block indices.
 template <int W32, int METHOD>
 __global__ void __launch_bounds__(32, ABIN_V5_MINB) k_mom5(const __grid_constant__ CUtensorMap tin, const MomParams p) {
+  // the dependent k_fixup grid (PDL) may be scheduled once every CTA has started
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int nE = p.sL + (p.n_strips - p.sR);
   const int64_t per_strip = (int64_t)p.n_bands * p.n_pages_v4;
   const int64_t te = (int64_t)nE * per_strip;

@@ -617,6 +617,7 @@ __device__ __forceinline__ void q5_body(const Q5Params& p, uint8_t* sm, int stri
 
 template <int WR, int NW>
 __global__ void __launch_bounds__(32, ABIN_Q5_MINB) k_quant5(const __grid_constant__ Q5Params p) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // k_q5fix (PDL) may be scheduled
   extern __shared__ __align__(16) uint8_t q5sm[];
   int64_t tile = blockIdx.x;
   const int strip = (int)(tile % p.n_strips);
@@ -634,6 +635,7 @@ __global__ void __launch_bounds__(32, ABIN_Q5_MINB) k_quant5(const __grid_consta
 // The exact queue: one warp per undecided pixel (exact_decide).
 static __global__ void __launch_bounds__(256) k_q5fix(const __grid_constant__ Q5Params p) {
   const int lane = threadIdx.x & 31;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic launch: k_quant5's queue and mask
   const uint32_t n_e = min(*p.fq_count, p.fq_cap);
   for (uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < n_e; e += (gridDim.x * blockDim.x) >> 5) {
     const uint4 q = p.fq[e];
