@@ -169,8 +169,14 @@ int abin_quantile(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uin
  * min, max = extrema of the in-bounds gray levels of the window; I' = 0 iff
  * I <= (min + max) / 2 (exact integer test 2 I <= min + max).  contrast >= 0
  * selects the local-contrast variant (same paragraph: "estimate local contrast
- * by range of gray levels"): I' = 1 where max - min < contrast.  Computed from
- * the sliding-histogram kernel of abin_quantile. */
+ * by range of gray levels"): I' = 1 where max - min < contrast.  Work per pixel
+ * is independent of h and w (the paragraph's Theta(HW)): separable running
+ * extrema by van Herk / Gil-Werman block prefix / suffix extrema, a row pass
+ * then a column pass with the decision.  Scratch: 4
+ * bytes per pixel from the stream-ordered pool (the row pass's (min, max)
+ * pairs and the column pass's suffix pairs), freed stream-ordered;
+ * ABIN_ENOMEM if it cannot be had.  ABIN_ERANGE beyond
+ * abin_limits().bernsen_max_window_w. */
 int abin_bernsen(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out, int64_t out_pitch,
                  int32_t mask_format, int32_t h, int32_t w, int32_t contrast, uint32_t flags, void* stream);
 
@@ -279,8 +285,9 @@ typedef struct {
   int64_t max_window_h;          /*   effective height (255^2 h < 2^32: column square sums in uint32) */
   int64_t max_window_hw;         /*   255 h w < 2^32 (window sums of I in uint32) */
   int64_t max_dim;               /* largest H or W, every method */
-  int64_t quantile_max_window_w; /* quantile / Bernsen: effective width */
+  int64_t quantile_max_window_w; /* quantile (and abin_stats of Bernsen): effective width */
   int64_t quantile_max_window_hw;/*   h w <= 65535 (16-bit histogram bins) */
+  int64_t bernsen_max_window_w;  /* Bernsen masks: effective width (any height) */
 } abin_limits_t;
 void abin_limits(abin_limits_t* out);
 const char* abin_strerror(int status);

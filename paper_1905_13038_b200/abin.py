@@ -60,7 +60,8 @@ _lib.abin_last_cuda_error.restype = ctypes.c_char_p
 
 class AbinLimits(ctypes.Structure):
     _fields_ = [("max_window_w", _I64), ("max_window_h", _I64), ("max_window_hw", _I64), ("max_dim", _I64),
-                ("quantile_max_window_w", _I64), ("quantile_max_window_hw", _I64)]
+                ("quantile_max_window_w", _I64), ("quantile_max_window_hw", _I64),
+                ("bernsen_max_window_w", _I64)]
 
 
 _lib.abin_limits.argtypes = [ctypes.POINTER(AbinLimits)]

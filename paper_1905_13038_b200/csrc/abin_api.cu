@@ -16,6 +16,7 @@
 #include "otsu.cuh"
 #include "fixup.cuh"
 #include "launch.cuh"
+#include "bernsen.cuh"
 #include "quantile.cuh"
 
 using namespace abin;
@@ -918,11 +919,86 @@ int run_quant5(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64
   return rc;
 }
 
+// Bernsen (method 4) masks: the window-independent separable extrema of
+// bernsen.cuh (row pass, then column pass with the decision).  Scratch: the
+// row pass's (min, 255 - max) pairs and the column pass's suffix pairs, 2
+// bytes per pixel each (an O(HW) departure from SURVEY 8(b), stated in abin.h).
+int run_bernsen(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64_t W, int64_t in_pitch, uint8_t* out,
+                int64_t out_pitch, int64_t out_page_stride, int32_t fmt, const Window& win, double contrast,
+                int64_t row0, int64_t H_out, int64_t H_global, int64_t buf_row0, cudaStream_t st) {
+  using namespace bern;
+  if (win.w > kBernMaxW) return ABIN_ERANGE;
+  BernParams p;
+  memset(&p, 0, sizeof(p));
+  p.in = in; p.in_page_stride = in_page_stride; p.in_pitch = in_pitch; p.W = W; p.buf_row0 = buf_row0;
+  p.row0 = row0; p.H_out = H_out; p.H_global = H_global;
+  p.out = out; p.out_pitch = out_pitch; p.out_page_stride = out_page_stride; p.fmt = fmt;
+  p.w = win.w; p.l = win.l; p.h = win.h; p.o = win.o;
+  p.contrast = (int32_t)std::max(-1.0, std::min(256.0, std::floor(contrast)));
+  p.Y0 = std::max<int64_t>(0, row0 - win.o + 1);
+  p.Yn = std::min<int64_t>(H_global, row0 + H_out + win.u) - p.Y0;
+  p.hpitch = (W + 7) / 8 * 8;
+  p.TW = win.w <= 384 ? 128 : 256;  // (w > TW: one block per tile, its suffix pass spans the window)
+  p.SP = (15 + p.TW + win.w + 15) / 16 * 16 + 4;
+  p.OBP = p.TW + 2;
+  p.n_ctiles = (int32_t)((W + p.TW - 1) / p.TW);
+  p.n_rtiles = (int32_t)((p.Yn + 31) / 32);
+  p.n_groups = (int32_t)((W + 7) / 8);
+  p.n_chunks = (int32_t)((H_out + win.h - 1) / win.h);
+  p.n_pages = (int32_t)n_pages;
+  const size_t hsm = (size_t)h_smem_bytes(p.SP, p.w, p.OBP);
+  if (hsm > 227 * 1024) return ABIN_ERANGE;
+  // column pass: split each chunk over R threads until ~1.2M threads are in
+  // flight (each keeps 4 row loads in flight); the local suffixes stay in
+  // shared memory (16 bytes per thread and row) unless the window is too tall
+  p.n_gblocks = (p.n_groups + 31) / 32;
+  const int64_t base = (int64_t)p.n_gblocks * 32 * p.n_chunks * n_pages;
+  int R = (int)std::max<int64_t>(1, std::min<int64_t>(8, (1200000 + base - 1) / std::max<int64_t>(1, base)));
+  R = std::min(R, win.h);
+  p.sbs = (win.h + R - 1) / R;
+  R = (win.h + p.sbs - 1) / p.sbs;
+  const size_t vsm_need = (size_t)R * 32 * p.sbs * 16;
+  const bool v_smem = vsm_need <= 96 * 1024 && !getenv("ABIN_BERN_GSB");  // (experiments: global sb)
+  const size_t vsm = v_smem ? vsm_need : 0;
+  void* scratch = nullptr;
+  const size_t hb_bytes = (size_t)n_pages * p.Yn * p.hpitch * 2;
+  const size_t sb_bytes = v_smem ? 0 : (size_t)n_pages * H_out * p.hpitch * 2;
+  if (cudaMallocAsync(&scratch, hb_bytes + sb_bytes, st) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return ABIN_ENOMEM;
+  }
+  p.hb = reinterpret_cast<uint16_t*>(scratch);
+  p.sb = v_smem ? nullptr : reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(scratch) + hb_bytes);
+  static bool attr_done[64] = {};
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if ((hsm > 48 * 1024 || vsm + sizeof(uint4) * 2 * 8 * 32 > 48 * 1024) && dev >= 0 && dev < 64 && !attr_done[dev]) {
+    CK(cudaFuncSetAttribute(k_bern_h, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    CK(cudaFuncSetAttribute(k_bern_v, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_done[dev] = true;
+  }
+  int rc = ABIN_OK;
+  const int64_t nh = (int64_t)p.n_ctiles * p.n_rtiles * n_pages;
+  const int64_t nv = (int64_t)p.n_gblocks * p.n_chunks * n_pages;
+  if (nh > 0 && nv > 0) {
+    k_bern_h<<<(unsigned)nh, 32, hsm, st>>>(p);
+    k_bern_v<<<(unsigned)nv, dim3(32, R), vsm, st>>>(p);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) rc = cuda_fail(e);
+  }
+  const cudaError_t f = cudaFreeAsync(scratch, st);
+  if (rc == ABIN_OK && f != cudaSuccess) return cuda_fail(f);
+  return rc;
+}
+
 int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64_t /*H_held*/, int64_t W,
                  int64_t in_pitch, uint8_t* out, int64_t out_pitch, int64_t out_page_stride, int32_t fmt, int32_t h,
                  int32_t w, double q, int64_t row0, int64_t H_out, int64_t H_global, int64_t buf_rows,
                  int64_t buf_row0, cudaStream_t st, double* Q_out, uint32_t flags, uint64_t* counters) {
   const Window win = effective_window(h, w, H_global, W);
+  if (method == ABIN_BERNSEN && !Q_out && !(flags & ABIN_Q2_INTERNAL))
+    return run_bernsen(in, in_page_stride, n_pages, W, in_pitch, out, out_pitch, out_page_stride, fmt, win, q, row0,
+                       H_out, H_global, buf_row0, st);
   // v5 (quantile5.cuh) for masks at q >= 0.2; low quantiles of document
   // pages sit in either the strokes' or the background's levels, which a few
   // 16-level windows per tile do not cover (measured: 1-35 % of the pixels to
@@ -1559,6 +1635,7 @@ void abin_limits(abin_limits_t* out) {
   out->max_dim = kMaxDim;
   out->quantile_max_window_w = 3 * kQuantNT + 1;  // a thread stages at most 4 elements of a row
   out->quantile_max_window_hw = 65535;            // u16 bins
+  out->bernsen_max_window_w = bern::kBernMaxW;    // the row pass's staged tile (no h or h w limit)
 }
 
 const char* abin_strerror(int status) {

@@ -140,10 +140,13 @@ def test_limits_match_the_erange_checks(lib):
     assert q(256, 256) == 3                                  # h w > 65535
     b = lambda h, w: raw.abin_binarize_batched(4, FAKE_IN, H * W, FAKE_OUT, H * W, 1, H, W, W, W, 0, h, w, -1.0, 0.0,
                                                -1, 0, None, None)
-    assert b(3, L.quantile_max_window_w + 1) == 3            # Bernsen shares the histogram kernels
+    assert L.bernsen_max_window_w == 2048
+    big = 1 << 20
+    bb = lambda h, w: raw.abin_binarize_batched(4, FAKE_IN, big, FAKE_OUT, big, 1, 8, big, big, big, 0, h, w, -1.0,
+                                                0.0, -1, 0, None, None)
+    assert bb(3, L.bernsen_max_window_w + 1) == 3            # Bernsen: the row pass's staged tile
     # moments: effective sizes are clamped to the image, so a huge window on a
     # big (fake) image exceeds the width limit
-    big = 1 << 20
     m = lambda h, w: raw.abin_binarize_batched(0, FAKE_IN, big, FAKE_OUT, big, 1, 8, big, big, big, 0, h, w, 0.5,
                                                128.0, -1, 0, None, None)
     assert m(3, L.max_window_w + 1) == 3

@@ -383,10 +383,11 @@ def test_host_io_row_bands(monkeypatch, method, p0, p1, L, packed, pad):
 @pytest.mark.parametrize("contrast", [-1, 15])
 @pytest.mark.parametrize("single", [False, True])
 def test_bernsen_small(monkeypatch, contrast, single):
-    """Bernsen midrange on the histogram kernels (the paired
-    k_quantile2 by default, k_quantile with ABIN_QUANTILE_SINGLE) vs the direct
-    extrema oracle: random and document images, odd/even windows, windows
-    larger than the image, byte and bit masks, tight and padded pitches."""
+    """Bernsen midrange: the window-independent row/column
+    kernels (default) and the histogram kernels (Q2_INTERNAL: the paired
+    k_quantile2, k_quantile with ABIN_QUANTILE_SINGLE) vs the direct extrema
+    oracle: random and document images, odd/even windows, windows larger than
+    the image, byte and bit masks, tight and padded pitches."""
     if single:
         monkeypatch.setenv("ABIN_QUANTILE_SINGLE", "1")
     rng = np.random.default_rng(contrast + 2)
@@ -398,8 +399,10 @@ def test_bernsen_small(monkeypatch, contrast, single):
             ref, lo, hi = oracle.bernsen(I, h, w, contrast)
             for pitch in (None, W):
                 x = to_dev(I, pitch)
-                assert np.array_equal(ab.bernsen(x, h, w, contrast).cpu().numpy(), ref)
-                assert np.array_equal(ab.bernsen(x, h, w, contrast, packed=True).cpu().numpy(), oracle.pack_bits(ref))
+                for fl in (0, abin.Q2_INTERNAL):
+                    assert np.array_equal(ab.bernsen(x, h, w, contrast, flags=fl).cpu().numpy(), ref)
+                    assert np.array_equal(ab.bernsen(x, h, w, contrast, packed=True, flags=fl).cpu().numpy(),
+                                          oracle.pack_bits(ref))
             s = ab.stats("bernsen", to_dev(I), h, w, float(contrast))
             assert np.array_equal(s["t"].cpu().numpy(), 0.5 * (lo.astype(np.float64) + hi))
             assert np.array_equal(s["mask"].cpu().numpy(), ref)
