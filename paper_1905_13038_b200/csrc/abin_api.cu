@@ -124,17 +124,18 @@ int launch_v4_any(int w32, bool d64, const CUtensorMap& map, const MomParams& p,
   return e == cudaSuccess ? ABIN_OK : cuda_fail(e);
 }
 
-int launch_v5_any(int w32, const CUtensorMap& map, const MomParams& p, int64_t n, cudaStream_t st) {
+int launch_v5_any(int w32, const CUtensorMap& map, const CUtensorMap& mpk, const MomParams& p, int64_t n,
+                  cudaStream_t st) {
   cudaError_t e = cudaErrorInvalidValue;
   switch (w32 >> 2) {
-    case 0: e = launch_v5_part0(w32, map, p, n, st); break;
-    case 1: e = launch_v5_part1(w32, map, p, n, st); break;
-    case 2: e = launch_v5_part2(w32, map, p, n, st); break;
-    case 3: e = launch_v5_part3(w32, map, p, n, st); break;
-    case 4: e = launch_v5_part4(w32, map, p, n, st); break;
-    case 5: e = launch_v5_part5(w32, map, p, n, st); break;
-    case 6: e = launch_v5_part6(w32, map, p, n, st); break;
-    case 7: e = launch_v5_part7(w32, map, p, n, st); break;
+    case 0: e = launch_v5_part0(w32, map, mpk, p, n, st); break;
+    case 1: e = launch_v5_part1(w32, map, mpk, p, n, st); break;
+    case 2: e = launch_v5_part2(w32, map, mpk, p, n, st); break;
+    case 3: e = launch_v5_part3(w32, map, mpk, p, n, st); break;
+    case 4: e = launch_v5_part4(w32, map, mpk, p, n, st); break;
+    case 5: e = launch_v5_part5(w32, map, mpk, p, n, st); break;
+    case 6: e = launch_v5_part6(w32, map, mpk, p, n, st); break;
+    case 7: e = launch_v5_part7(w32, map, mpk, p, n, st); break;
   }
   return e == cudaSuccess ? ABIN_OK : cuda_fail(e);
 }
@@ -442,7 +443,7 @@ int encode_map(const MomCall& c, int box_rows, bool tma_ok, CUtensorMap* map) {
 // v4 view of the pages: {16 bytes, ceil(W/16) chunks, rows, pages}; a box is
 // `chunks` whole chunks x `rows` rows (moments4.cuh).  Needs 16-byte aligned
 // base, pitch and page stride.
-int encode_map_chunks(const MomCall& c, int chunks, int rows, CUtensorMap* map) {
+int encode_map_chunks(const MomCall& c, int chunks, int rows, CUtensorMap* map, int box_pages = 1) {
   memset(map, 0, sizeof(*map));
   PFN_encodeTiled enc = get_encode();
   if (!enc) {
@@ -452,7 +453,7 @@ int encode_map_chunks(const MomCall& c, int chunks, int rows, CUtensorMap* map) 
   cuuint64_t dims[4] = {16, (cuuint64_t)((c.W + 15) / 16), (cuuint64_t)c.buf_rows, (cuuint64_t)c.n_pages};
   cuuint64_t strides[3] = {16, (cuuint64_t)c.in_pitch,
                            (cuuint64_t)(c.n_pages > 1 ? c.in_page_stride : c.in_pitch * c.buf_rows)};
-  cuuint32_t box[4] = {16, (cuuint32_t)chunks, (cuuint32_t)rows, 1};
+  cuuint32_t box[4] = {16, (cuuint32_t)chunks, (cuuint32_t)rows, (cuuint32_t)box_pages};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult cr = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(c.in), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -638,7 +639,27 @@ int run_moments(const MomCall& c) {
       q.sL = (int32_t)sL;
       q.sR = (int32_t)std::max<int64_t>(sL, std::min<int64_t>(nfit, q.n_strips));
       q.n_pages_v4 = (int32_t)c.n_pages;
-      choose_bands_v4((int64_t)q.n_strips * c.n_pages, c.H_out, win.h,
+      // Packed last strips (v5, page batches): when the last strip of a page
+      // holds only a few output lanes (config 3: 32 of 448 columns), the last
+      // strips of NG pages share one warp -- G = KH + its output lanes each,
+      // one TMA box of NG pages -- instead of a mostly idle warp per page
+      CUtensorMap mpk = map4;
+      if (use_v5 && c.method != M_MAXS && c.n_pages >= 2 && q.n_strips >= 2 && !getenv("ABIN_NO_PACK")) {
+        const int64_t rem = c.W - (int64_t)(q.n_strips - 1) * q.Tw;  // outputs of the last strip
+        const int G = q.KH + (int)((rem + kG - 1) / kG);
+        const int NG = std::min(32 / G, v5::kRowsBytes / (v5::kR * kG * (G + 1)));
+        if (NG >= 2 && q.sR <= q.n_strips - 1 && q.sL <= q.n_strips - 1) {
+          rc = encode_map_chunks(c, G + 1, v5::kR, &mpk, NG);
+          if (rc != ABIN_OK) return rc;
+          q.pk_on = 1;
+          q.pk_G = G;
+          q.pk_NG = NG;
+          q.pk_n = (int32_t)((c.n_pages + NG - 1) / NG);
+        }
+      }
+      const int64_t col_tiles = q.pk_on ? (int64_t)(q.n_strips - 1) * c.n_pages + q.pk_n
+                                        : (int64_t)q.n_strips * c.n_pages;
+      choose_bands_v4(col_tiles, c.H_out, win.h,
                       num_sms() * (use_v5 ? occupancy_v5_any(win.w % 32, c.method) : warp_cta_slots(v4::smem_bytes())),
                       &q.B, &q.n_bands);
       if (const char* nb = getenv("ABIN_V4_BANDS")) {  // experiments: force the band count
@@ -660,7 +681,8 @@ int run_moments(const MomCall& c) {
       q.q_data = queue;
       q.q_count = qcount;
       q.q_cap = cap;
-      const int64_t n_tiles = (int64_t)q.n_strips * q.n_bands * c.n_pages;
+      const int64_t n_tiles = q.pk_on ? ((int64_t)(q.n_strips - 1) * c.n_pages + q.pk_n) * q.n_bands
+                                      : (int64_t)q.n_strips * q.n_bands * c.n_pages;
       if (c.method == M_MAXS) {
         // Wolf's adaptive R (R21): pass 0 = max v~ per page, pass 1 = the
         // pixels within 2 |v~ - v| of it (the true maximum is among them),
@@ -677,16 +699,17 @@ int run_moments(const MomCall& c) {
         q.smax_bits = c.smax_out;
         q.maxs_margin = 2.05f * q.rdv;
         q.maxs_pass = 0;
-        rc = launch_v5_any(w32, map4, q, n_tiles, c.stream);
+        rc = launch_v5_any(w32, map4, map4, q, n_tiles, c.stream);
         q.maxs_pass = 1;
-        if (rc == ABIN_OK) rc = launch_v5_any(w32, map4, q, n_tiles, c.stream);
+        if (rc == ABIN_OK) rc = launch_v5_any(w32, map4, map4, q, n_tiles, c.stream);
         if (rc == ABIN_OK) rc = launch_fixup(q, win.w, c.stream);
         cudaError_t e1 = cudaFreeAsync(vmax, c.stream), e2 = cudaFreeAsync(queue, c.stream);
         if (rc == ABIN_OK && e1 != cudaSuccess) return cuda_fail(e1);
         if (rc == ABIN_OK && e2 != cudaSuccess) return cuda_fail(e2);
         return rc;
       }
-      rc = use_v5 ? launch_v5_any(w32, map4, q, n_tiles, c.stream) : launch_v4_any(w32, d64, map4, q, n_tiles, c.stream);
+      rc = use_v5 ? launch_v5_any(w32, map4, mpk, q, n_tiles, c.stream)
+                  : launch_v4_any(w32, d64, map4, q, n_tiles, c.stream);
       if (rc == ABIN_OK) rc = launch_fixup(q, win.w, c.stream);
       if (rc == ABIN_OK && may_overflow) {
         // overflow (pathological inputs only): the v3 kernel redoes the call

@@ -40,7 +40,8 @@ cudaError_t launch_wide(bool d64, bool stats, int nt, int ph, const CUtensorMap&
                                   cudaStream_t st);                                                         \
   cudaError_t launch_v4_part##k(int w32, bool d64, const CUtensorMap& map, const MomParams& p, int64_t n,   \
                                 cudaStream_t st);                                                           \
-  cudaError_t launch_v5_part##k(int w32, const CUtensorMap& map, const MomParams& p, int64_t n, cudaStream_t st); \
+  cudaError_t launch_v5_part##k(int w32, const CUtensorMap& map, const CUtensorMap& mpk, const MomParams& p,       \
+                                int64_t n, cudaStream_t st);                                                      \
   int occupancy_v5_part##k(int w32, int method);
 ABIN_DECL_PART(0) ABIN_DECL_PART(1) ABIN_DECL_PART(2) ABIN_DECL_PART(3)
 ABIN_DECL_PART(4) ABIN_DECL_PART(5) ABIN_DECL_PART(6) ABIN_DECL_PART(7)

@@ -76,6 +76,9 @@ struct MomParams {
   const uint32_t* ovf_count;
   uint32_t ovf_cap;
   int32_t n_pages_v4;        // v4: pages of the launch
+  // v5 packed last strips: the last strip of NG pages in one warp, G lanes
+  // each (KH halo + its output lanes), staged by one TMA box of NG pages
+  int32_t pk_on, pk_G, pk_NG, pk_n;  // pk_n: packs per band = ceil(pages / NG)
   // M_MAXS (Wolf's image-adaptive R = max s, R21): pass 0 reduces the
   // fp32 v~ per page into vmax_bits; pass 1 queues the pixels whose v~ is within
   // maxs_margin (>= 2 |v~ - v| bound) of it; k_fixup takes their exact fp64 s

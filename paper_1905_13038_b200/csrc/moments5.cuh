@@ -238,8 +238,13 @@ __global__ void k_probe(const uint32_t* c, const uint32_t* d, const uint32_t* nc
 //         columns in the published row
 //   EDGE  strips whose windows reach the left/right border (per-column counts,
 //         bytes past W masked); false: interior strips [sL, sR)
-template <int W32, int METHOD, bool EDGE>
-__device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParams& p, int strip, int band, int page) {
+//   PACK  the packed last strips (implies EDGE): lane = (group grp, lane kl of
+//         G in the group), group grp = the last strip of page pack NG + grp,
+//         all staged by one TMA box of NG pages x (G + 1) chunks (tin is
+//         then the packed tensor map); a group is a strip of G lanes
+template <int W32, int METHOD, bool EDGE, bool PACK = false>
+__device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParams& p, int strip, int band,
+                                          int page_arg) {
   constexpr int W16 = W32 & 15;
   constexpr int DL = (W32 >> 1) & 15;      // r mod 16
   constexpr int RHO = (16 - W16) & 15;     // (-w) mod 16
@@ -250,6 +255,14 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
 
   const int lane = threadIdx.x;
   const int KH = p.KH;
+  // packed strips: the lane's group and its place in it
+  const int G = PACK ? p.pk_G : 32;
+  const int grp = PACK ? lane / G : 0;
+  const int kl = PACK ? lane - grp * G : lane;               // lane within its strip
+  const int page = PACK ? page_arg * p.pk_NG + grp : page_arg;
+  const bool lane_ok = !PACK || (grp < p.pk_NG && page < p.n_pages_v4);
+  const int RS = PACK ? kG * (G + 1) : kSpan;                // staged row stride
+  const int page0 = PACK ? page_arg * p.pk_NG : page_arg;    // TMA page coordinate
   const int64_t J0 = (int64_t)strip * p.Tw;               // first output column of the strip
   const int64_t Sw = J0 + p.r - (int64_t)kG * KH;         // input column of lane 0
   const int64_t XE = Sw - DL;                             // 16-aligned staging origin
@@ -265,26 +278,26 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
     uint8_t* st = ring + slot * kStageBytes;
     const uint64_t keep = (ABIN_V5_L2 & 2) ? policy_evict_normal() : policy_evict_last();
     const uint64_t drop = (ABIN_V5_L2 & 4) ? policy_evict_normal() : policy_evict_first();
-    mbar_arrive_expect_tx(&full[slot], 2 * kR * kSpan);
+    mbar_arrive_expect_tx(&full[slot], 2 * kR * RS * (PACK ? p.pk_NG : 1));
     if (s < WS) {  // warm-up rows y0-o+2kR s .. +2kR-1 into both halves of the slot
       const int32_t yw = (int32_t)(y0 - p.o + (int64_t)s * 2 * kR - p.buf_row0);
-      tma_load_4d_hint(st, &tin, 0, xchunk, yw, page, &full[slot], keep);
-      tma_load_4d_hint(st + kRowsBytes, &tin, 0, xchunk, yw + kR, page, &full[slot], keep);
+      tma_load_4d_hint(st, &tin, 0, xchunk, yw, page0, &full[slot], keep);
+      tma_load_4d_hint(st + kRowsBytes, &tin, 0, xchunk, yw + kR, page0, &full[slot], keep);
     } else {
       const int64_t q0 = (int64_t)(s - WS) * kR;
-      tma_load_4d_hint(st, &tin, 0, xchunk, (int32_t)(y0 + q0 + p.u - p.buf_row0), page, &full[slot], keep);
-      tma_load_4d_hint(st + kRowsBytes, &tin, 0, xchunk, (int32_t)(y0 + q0 - p.o - p.buf_row0), page, &full[slot],
+      tma_load_4d_hint(st, &tin, 0, xchunk, (int32_t)(y0 + q0 + p.u - p.buf_row0), page0, &full[slot], keep);
+      tma_load_4d_hint(st + kRowsBytes, &tin, 0, xchunk, (int32_t)(y0 + q0 - p.o - p.buf_row0), page0, &full[slot],
                        drop);
     }
   };
 
   // ---- per-lane geometry
-  const int64_t a = Sw + (int64_t)kG * lane;              // first owned input column
+  const int64_t a = Sw + (int64_t)kG * kl;                // first owned input column
   const int64_t j0 = a - p.r;                             // first output column (multiple of 16)
-  const int64_t Jend = min(J0 + p.Tw, p.W);
-  const bool valid_lane = lane >= KH && j0 < Jend;
+  const int64_t Jend = min(J0 + (PACK ? (int64_t)kG * (G - KH) : (int64_t)p.Tw), p.W);
+  const bool valid_lane = lane_ok && kl >= KH && j0 < Jend;
   const uint32_t vmask = valid_lane ? (Jend - j0 >= kG ? 0xFFFFu : ((1u << (uint32_t)(Jend - j0)) - 1u)) : 0u;
-  const float Lf = (METHOD == M_WOLF) ? (float)(p.L_fixed >= 0 ? p.L_fixed : (int)p.L_page[page]) : 0.0f;
+  const float Lf = (METHOD == M_WOLF) ? (float)(p.L_fixed >= 0 ? p.L_fixed : (lane_ok ? (int)p.L_page[page] : 0)) : 0.0f;
   // Edge strips.  (1) -1/ncol per output column: ncol = w
   // except within (w+1)/2 columns of a border, so at most 10 lanes of a strip
   // see other counts; they get their own 16-entry slot of the table, every
@@ -340,8 +353,10 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
         const int c0 = tail_off & ~15, nb = tail_off & 15;
         uint8_t* st = ring + (s % kNS) * kStageBytes;
 #pragma unroll 1
-        for (int z = 0; z < 2 * kR; ++z) {
-          uint4* q = reinterpret_cast<uint4*>(st + (z < kR ? z * kSpan : kRowsBytes + (z - kR) * kSpan) + c0);
+        for (int z = 0; z < 2 * kR * (PACK ? p.pk_NG : 1); ++z) {
+          const int zg = PACK ? z / (2 * kR) : 0, zr = PACK ? z - zg * 2 * kR : z;
+          uint4* q = reinterpret_cast<uint4*>(st + (zr < kR ? zr * RS : kRowsBytes + (zr - kR) * RS) +
+                                              zg * kR * RS + c0);
           uint4 v = *q;
           uint32_t* vw = reinterpret_cast<uint32_t*>(&v);
 #pragma unroll
@@ -363,7 +378,7 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
 #pragma unroll
   for (int q = 0; q < 8; ++q) SC[q] = SD[q] = splat(8388608.0f);
   const f2 M32 = splat(-32768.0f), M64 = splat(-65536.0f);
-  const int eo = kG * lane;  // staged offset of the lane's 32-byte window
+  const int eo = PACK ? grp * kR * RS + kG * kl : kG * lane;  // staged offset of the lane's 32-byte window
 
   // ---- warm-up: rows y0-o .. y0+u-1
   for (int s = 0; s < WS; ++s) {
@@ -373,7 +388,7 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
 #pragma unroll 1
     for (int rr = 0; rr < nr; ++rr) {
       uint32_t w[8];
-      load_row(st + (rr < kR ? rr * kSpan : kRowsBytes + (rr - kR) * kSpan), w);
+      load_row(st + (rr < kR ? rr * RS : kRowsBytes + (rr - kR) * RS), w);
 #define ABIN_V5_WU(P)                                                                          \
   {                                                                                            \
     const f2 x = add2(pk(own_f<DL, 2 * P>(w), own_f<DL, 2 * P + 1>(w)), M32);                 \
@@ -389,7 +404,7 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
 
   // centre rows (the pixels decided): one 16-byte load per lane per row, one row ahead
   const int64_t cx = j0;
-  const int cmode = (cx >= 0 && cx + kG <= p.W) ? 1 : ((cx >= 0 && cx < p.W) ? 2 : 0);
+  const int cmode = !lane_ok ? 0 : ((cx >= 0 && cx + kG <= p.W) ? 1 : ((cx >= 0 && cx < p.W) ? 2 : 0));
   const uint8_t* cptr = p.in + (int64_t)page * p.in_page_stride + (y0 - p.buf_row0) * p.in_pitch + cx;
   auto load_centre = [&](const uint8_t* src) -> uint4 {
     if (cmode == 0) return make_uint4(0, 0, 0, 0);
@@ -440,8 +455,8 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
       // ---- vertical update, exact in fp32
       {
         uint32_t wi[8], wo[8];
-        load_row(st + rr * kSpan, wi);
-        load_row(st + kRowsBytes + rr * kSpan, wo);
+        load_row(st + rr * RS, wi);
+        load_row(st + kRowsBytes + rr * RS, wo);
 #define ABIN_V5_VU(P)                                                                                 \
   {                                                                                                   \
     const f2 fi = pk(own_f<DL, 2 * P>(wi), own_f<DL, 2 * P + 1>(wi));                                 \
@@ -625,20 +640,29 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
 
 // One launch for all strips: the border strips get the low block indices.
 template <int W32, int METHOD>
-__global__ void __launch_bounds__(32, ABIN_V5_MINB) k_mom5(const __grid_constant__ CUtensorMap tin, const MomParams p) {
+__global__ void __launch_bounds__(32, ABIN_V5_MINB) k_mom5(const __grid_constant__ CUtensorMap tin,
+                                                           const __grid_constant__ CUtensorMap tpk, const MomParams p) {
   // the dependent k_fixup grid (PDL) may be scheduled once every CTA has started
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int nE = p.sL + (p.n_strips - p.sR);
+  // tiles: the edge strips (less the last strip when it is packed), then the
+  // packed last strips (pk_n per band), then the interior strips
+  const int nE = p.sL + (p.n_strips - (p.pk_on ? 1 : 0) - p.sR);
   const int64_t per_strip = (int64_t)p.n_bands * p.n_pages_v4;
   const int64_t te = (int64_t)nE * per_strip;
+  const int64_t tp = p.pk_on ? (int64_t)p.pk_n * p.n_bands : 0;
   int64_t tile = blockIdx.x;
   if (tile < te) {
     const int si = (int)(tile % nE);
     tile /= nE;
     const int strip = si < p.sL ? si : p.sR + (si - p.sL);
     mom5_body<W32, METHOD, true>(tin, p, strip, (int)(tile % p.n_bands), (int)(tile / p.n_bands));
+  } else if (tile < te + tp) {
+    if constexpr (METHOD != M_MAXS) {  // (the host packs no M_MAXS launch)
+      tile -= te;
+      mom5_body<W32, METHOD, true, true>(tpk, p, p.n_strips - 1, (int)(tile % p.n_bands), (int)(tile / p.n_bands));
+    }
   } else {
-    tile -= te;
+    tile -= te + tp;
     const int nI = p.sR - p.sL;
     const int strip = p.sL + (int)(tile % nI);
     tile /= nI;

@@ -33,13 +33,14 @@ cudaError_t launch_v4_m(const CUtensorMap& map, const MomParams& p, int64_t n_ti
 }
 
 template <int W32, int METHOD>
-cudaError_t launch_v5_m(const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st) {
+cudaError_t launch_v5_m(const CUtensorMap& map, const CUtensorMap& mpk, const MomParams& p, int64_t n_tiles,
+                        cudaStream_t st) {
   constexpr size_t smem = v5::smem_bytes();
   auto kern = v5::k_mom5<W32, METHOD>;
   static bool attr_set[64] = {};
   const cudaError_t e = set_smem_attr_once(kern, smem, attr_set);
   if (e != cudaSuccess) return e;
-  if (n_tiles > 0) kern<<<(unsigned)n_tiles, 32, smem, st>>>(map, p);
+  if (n_tiles > 0) kern<<<(unsigned)n_tiles, 32, smem, st>>>(map, mpk, p);
   return cudaGetLastError();
 }
 
@@ -69,13 +70,14 @@ int occ_v5(int method) {
 }
 
 template <int W32>
-cudaError_t launch_v5(const CUtensorMap& map, const MomParams& p, int64_t n_tiles, cudaStream_t st) {
-  if (p.method == M_SAUVOLA) return launch_v5_m<W32, M_SAUVOLA>(map, p, n_tiles, st);
-  if (p.method == M_NIBLACK) return launch_v5_m<W32, M_NIBLACK>(map, p, n_tiles, st);
-  if (p.method == M_MAXS) return launch_v5_m<W32, M_MAXS>(map, p, n_tiles, st);
-  if (p.method == M_KHURSHID) return launch_v5_m<W32, M_KHURSHID>(map, p, n_tiles, st);
-  if (p.method == M_PHANSALKAR) return launch_v5_m<W32, M_PHANSALKAR>(map, p, n_tiles, st);
-  return launch_v5_m<W32, M_WOLF>(map, p, n_tiles, st);
+cudaError_t launch_v5(const CUtensorMap& map, const CUtensorMap& mpk, const MomParams& p, int64_t n_tiles,
+                      cudaStream_t st) {
+  if (p.method == M_SAUVOLA) return launch_v5_m<W32, M_SAUVOLA>(map, mpk, p, n_tiles, st);
+  if (p.method == M_NIBLACK) return launch_v5_m<W32, M_NIBLACK>(map, mpk, p, n_tiles, st);
+  if (p.method == M_MAXS) return launch_v5_m<W32, M_MAXS>(map, mpk, p, n_tiles, st);
+  if (p.method == M_KHURSHID) return launch_v5_m<W32, M_KHURSHID>(map, mpk, p, n_tiles, st);
+  if (p.method == M_PHANSALKAR) return launch_v5_m<W32, M_PHANSALKAR>(map, mpk, p, n_tiles, st);
+  return launch_v5_m<W32, M_WOLF>(map, mpk, p, n_tiles, st);
 }
 
 template <int W32, bool D64>
@@ -98,14 +100,14 @@ cudaError_t ABIN_CAT(launch_v4_part, ABIN_PART)(int w32, bool d64, const CUtenso
   return cudaErrorInvalidValue;
 }
 
-cudaError_t ABIN_CAT(launch_v5_part, ABIN_PART)(int w32, const CUtensorMap& map, const MomParams& p, int64_t n,
-                                                cudaStream_t st) {
+cudaError_t ABIN_CAT(launch_v5_part, ABIN_PART)(int w32, const CUtensorMap& map, const CUtensorMap& mpk,
+                                                const MomParams& p, int64_t n, cudaStream_t st) {
   constexpr int b = 4 * ABIN_PART;
   switch (w32 - b) {
-    case 0: return launch_v5<b + 0>(map, p, n, st);
-    case 1: return launch_v5<b + 1>(map, p, n, st);
-    case 2: return launch_v5<b + 2>(map, p, n, st);
-    case 3: return launch_v5<b + 3>(map, p, n, st);
+    case 0: return launch_v5<b + 0>(map, mpk, p, n, st);
+    case 1: return launch_v5<b + 1>(map, mpk, p, n, st);
+    case 2: return launch_v5<b + 2>(map, mpk, p, n, st);
+    case 3: return launch_v5<b + 3>(map, mpk, p, n, st);
   }
   return cudaErrorInvalidValue;
 }
