@@ -65,7 +65,11 @@ if __name__ == "__main__":
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     sj = os.path.join(ROOT, "profiles", "ncu_summary.json")
     summary = json.load(open(sj)) if os.path.exists(sj) else {}
-    cfgs = {"c3": (3, 64 * 7016 * 4960, 2.0), "c4": (4, 32768 * 32768, 1.125), "c5": (5, 4096 * 4096, 2.0)}
+    # (label, px per launch, algorithmic bytes per px): the Bernsen row pass reads
+    # the page and writes its (min, max) pairs (1 + 2 B/px), the column pass reads
+    # the pairs and the centre pixels and writes the mask (2 + 1 + 1 B/px)
+    cfgs = {"c3": (3, 64 * 7016 * 4960, 2.0), "c4": (4, 32768 * 32768, 1.125), "c5": (5, 4096 * 4096, 2.0),
+            "bh": ("bernsen_row_pass", 4096 * 4096, 3.0), "bv": ("bernsen_column_pass", 4096 * 4096, 4.0)}
     for key, (cfg, px, bpp) in cfgs.items():
         raw = os.path.join(prof, f"{tag}_{key}_raw.csv")
         if not os.path.exists(raw):
@@ -73,7 +77,7 @@ if __name__ == "__main__":
         text, js = summarize(tag, cfg, raw, px, bpp)
         open(os.path.join(ROOT, "profiles", f"{tag}_ncu_{key}.txt"), "w").write(text)
         js["round"] = tag
-        summary[f"config{cfg}"] = js
+        summary[f"config{cfg}" if isinstance(cfg, int) else cfg] = js
         print(text)
     lc = os.path.join(prof, f"{tag}_launches_c3.csv")
     if os.path.exists(lc):
