@@ -17,6 +17,7 @@
 #include "fixup.cuh"
 #include "launch.cuh"
 #include "bernsen.cuh"
+#include "small.cuh"
 #include "quantile.cuh"
 
 using namespace abin;
@@ -490,6 +491,70 @@ static void keep_pool_warm() {
 
 int launch_fixup(const MomParams& q, int w, cudaStream_t st);
 
+// The small-call path (small.cuh): one launch of k_small for single small
+// pages -- tiles in shared memory, certified fp32 decision with the double
+// threshold inline, no fixup launch.  Returns -1 (nothing launched) when the
+// call is not one it takes.
+int run_small(const MomCall& c, const Window& win) {
+  using namespace sm;
+  const bool stats = c.c_out || c.d_out || c.n_out || c.t_out || c.mask_out;
+  const uint32_t forced = ABIN_FORCE_FP64 | ABIN_FORCE_U64_SQ | ABIN_V3_INTERNAL | ABIN_V4_INTERNAL |
+                          ABIN_NO_TMA_INTERNAL;
+  const char* px_env = getenv("ABIN_SMALL_PX");  // tests / experiments: the size limit (0: off)
+  const int64_t max_px = px_env ? atoll(px_env) : (int64_t)1 << 19;
+  if (stats || (c.flags & forced) || win.h > kMaxWin || win.w > kMaxWin ||
+      !(c.method == M_SAUVOLA || c.method == M_NIBLACK || c.method == M_WOLF) ||
+      c.n_pages * c.H_out * c.W > max_px)
+    return -1;
+  SmallParams p;
+  memset(&p, 0, sizeof(p));
+  p.in = c.in; p.in_page_stride = c.in_page_stride; p.in_pitch = c.in_pitch; p.W = c.W;
+  p.buf_row0 = c.buf_row0; p.row0 = c.row0; p.H_out = c.H_out; p.H_global = c.H_global;
+  p.out = c.out; p.out_pitch = c.out_pitch; p.out_page_stride = c.out_page_stride; p.fmt = c.fmt;
+  p.h = win.h; p.w = win.w; p.l = win.l; p.r = win.r; p.o = win.o; p.u = win.u;
+  p.RWp = (kTW + win.w - 1 + 3) / 4 * 4 + 1;
+  p.n_rt = (int32_t)((c.H_out + kTH - 1) / kTH);
+  p.n_ct = (int32_t)((c.W + kTW - 1) / kTW);
+  const FilterConsts f5 = filter_consts_v5(c.method, c.k, c.R, c.rprm);
+  p.fa = f5.fa; p.fb = f5.fb; p.delta1 = f5.delta1;
+  p.k = c.k; p.R = c.R;
+  p.L_fixed = c.L_override;
+  p.counters = reinterpret_cast<unsigned long long*>(c.counters);
+  unsigned int* Lw = nullptr;
+  if (c.method == M_WOLF && c.L_override < 0) {
+    CK(cudaMallocAsync(&Lw, (size_t)c.n_pages * 4 + (size_t)c.n_pages, c.stream));
+    uint8_t* l8 = reinterpret_cast<uint8_t*>(Lw + c.n_pages);
+    k_fill_u32<<<(unsigned)((c.n_pages + 255) / 256), 256, 0, c.stream>>>(Lw, c.n_pages, 0xFFu);
+    k_global_min<<<dim3((unsigned)num_sms(), (unsigned)c.n_pages), 256, 0, c.stream>>>(c.in, c.in_page_stride, c.H_out,
+                                                                                      c.W, c.in_pitch, Lw);
+    k_narrow_u8<<<(unsigned)((c.n_pages + 255) / 256), 256, 0, c.stream>>>(Lw, l8, c.n_pages);
+    p.L_page = l8;
+  }
+  const size_t smem = smem_bytes(p.RWp, win.h);
+  static bool attr[3][64] = {};
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const int mi = c.method == M_SAUVOLA ? 0 : (c.method == M_NIBLACK ? 1 : 2);
+  const void* kern = mi == 0 ? (const void*)k_small<M_SAUVOLA>
+                             : (mi == 1 ? (const void*)k_small<M_NIBLACK> : (const void*)k_small<M_WOLF>);
+  if (dev >= 0 && dev < 64 && !attr[mi][dev]) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr[mi][dev] = true;
+  }
+  void* args[] = {&p};
+  const int64_t n = (int64_t)p.n_rt * p.n_ct * c.n_pages;
+  int rc = ABIN_OK;
+  if (n > 0) {
+    const cudaError_t e = cudaLaunchKernel(kern, dim3((unsigned)n), dim3(sm::kNT), args, smem, c.stream);
+    if (e != cudaSuccess) rc = cuda_fail(e);
+  }
+  if (Lw) {
+    const cudaError_t f = cudaFreeAsync(Lw, c.stream);
+    if (rc == ABIN_OK && f != cudaSuccess) return cuda_fail(f);
+  }
+  return rc;
+}
+
 int run_moments(const MomCall& c) {
   keep_pool_warm();
   const Window win = effective_window(c.h, c.w, c.H_global, c.W);
@@ -502,6 +567,10 @@ int run_moments(const MomCall& c) {
   // generic loader stages the rows.
   const bool tma_ok = !((reinterpret_cast<uintptr_t>(c.in) & 15u) || (c.in_pitch & 15) ||
                         (c.n_pages > 1 && (c.in_page_stride & 15))) && !(c.flags & ABIN_NO_TMA_INTERNAL);
+  if (fast && (uint64_t)255 * (uint64_t)win.h * (uint64_t)win.w < (1ull << 32)) {
+    const int rs = run_small(c, win);  // single small pages: the one-launch tile kernel
+    if (rs >= 0) return rs;
+  }
   if (!tma_ok && fast && !(c.flags & ABIN_NO_TMA_INTERNAL)) {
     // Rows TMA cannot stage (unaligned base, pitch or page stride, e.g. a tight
     // 2550-byte row): re-pitch them into a 16-byte aligned scratch copy (one
