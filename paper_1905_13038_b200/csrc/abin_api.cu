@@ -512,7 +512,8 @@ int run_small(const MomCall& c, const Window& win) {
   p.buf_row0 = c.buf_row0; p.row0 = c.row0; p.H_out = c.H_out; p.H_global = c.H_global;
   p.out = c.out; p.out_pitch = c.out_pitch; p.out_page_stride = c.out_page_stride; p.fmt = c.fmt;
   p.h = win.h; p.w = win.w; p.l = win.l; p.r = win.r; p.o = win.o; p.u = win.u;
-  p.RWp = (kTW + win.w - 1 + 3) / 4 * 4 + 1;
+  p.RWp = (kTW + win.w - 1 + 15 + 15) / 16 * 16;
+  p.CWp = (kTW + win.w + 3) / 4 * 4 + 1;
   p.n_rt = (int32_t)((c.H_out + kTH - 1) / kTH);
   p.n_ct = (int32_t)((c.W + kTW - 1) / kTW);
   const FilterConsts f5 = filter_consts_v5(c.method, c.k, c.R, c.rprm);
@@ -530,7 +531,7 @@ int run_small(const MomCall& c, const Window& win) {
     k_narrow_u8<<<(unsigned)((c.n_pages + 255) / 256), 256, 0, c.stream>>>(Lw, l8, c.n_pages);
     p.L_page = l8;
   }
-  const size_t smem = smem_bytes(p.RWp, win.h);
+  const size_t smem = smem_bytes(p.RWp, p.CWp, win.h);
   static bool attr[3][64] = {};
   int dev = 0;
   CK(cudaGetDevice(&dev));

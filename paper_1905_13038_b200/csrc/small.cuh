@@ -37,7 +37,8 @@ struct SmallParams {
   int64_t out_pitch, out_page_stride;
   int32_t fmt;
   int32_t h, w, l, r, o, u;
-  int32_t RWp;                // region row pitch in shared memory (bytes / words), >= 128 + w - 1
+  int32_t RWp;                // region row pitch in shared memory (bytes, multiple of 16, >= 128 + w - 1 + 15)
+  int32_t CWp;                // pitch of the column sums (words, odd)
   int32_t n_rt, n_ct;         // tiles per page
   float fa, fb, delta1;
   double k, R;
@@ -47,9 +48,9 @@ struct SmallParams {
 };
 
 // region bytes rounded up to 16 (the sums that follow are 32-bit words)
-__host__ __device__ inline size_t region_bytes(int RWp, int h) { return ((size_t)(kTH + h - 1) * RWp + 15) & ~(size_t)15; }
-__host__ __device__ inline size_t smem_bytes(int RWp, int h) {
-  return region_bytes(RWp, h) + (size_t)2 * kTH * RWp * 4;
+__host__ __device__ inline size_t region_bytes(int RWp, int h) { return (size_t)(kTH + h - 1) * RWp; }
+__host__ __device__ inline size_t smem_bytes(int RWp, int CWp, int h) {
+  return region_bytes(RWp, h) + (size_t)2 * kTH * CWp * 4;
 }
 
 template <int METHOD>
@@ -62,25 +63,39 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
   const int rt = (int)(b % p.n_rt);
   const int page = (int)(b / p.n_rt);
   const int64_t i0 = p.row0 + (int64_t)rt * kTH, j0 = (int64_t)ct * kTW;
-  const int RH = kTH + p.h - 1, RW = kTW + p.w - 1, RWp = p.RWp;
+  const int RH = kTH + p.h - 1, RW = kTW + p.w - 1, RWp = p.RWp, CWp = p.CWp;
   uint8_t* reg = smem;                                                 // [RH][RWp]
-  uint32_t* Cs = reinterpret_cast<uint32_t*>(smem + region_bytes(RWp, p.h));  // [kTH][RWp]
-  uint32_t* Ds = Cs + kTH * RWp;
+  uint32_t* Cs = reinterpret_cast<uint32_t*>(smem + region_bytes(RWp, p.h));  // [kTH][CWp]
+  uint32_t* Ds = Cs + kTH * CWp;
   const uint8_t* pg = p.in + (int64_t)page * p.in_page_stride;
   const int64_t y0 = i0 - p.o + 1, x0 = j0 - p.l + 1;                 // region origin (global)
 
-  // 1. the region, 0 outside the image (or outside the held rows): warp wi
-  // takes rows wi, wi + 8, ..., its lanes consecutive columns
+  // 1. the region, 0 outside the image (or outside the held rows), staged
+  // from the 16-aligned column xa = x0 - dx: 16-byte chunks (byte loads only
+  // for chunks that leave the image or rows that are not 16-aligned)
+  const int64_t xa = x0 & ~(int64_t)15;
+  const int dx = (int)(x0 - xa);
   {
-    const int lane = tid & 31, wi = tid >> 5;
-    for (int ry = wi; ry < RH; ry += kNT / 32) {
-      const int64_t y = y0 + ry;
-      const bool yin = y >= 0 && y < p.H_global;
-      const uint8_t* row = pg + (y - p.buf_row0) * p.in_pitch;
-      for (int rx = lane; rx < RW; rx += 32) {
-        const int64_t x = x0 + rx;
-        reg[ry * RWp + rx] = (yin && x >= 0 && x < p.W) ? __ldg(row + x) : (uint8_t)0;
+    const int nch = (dx + RW + 15) >> 4;
+    const bool vec = ((reinterpret_cast<uintptr_t>(p.in) | (uintptr_t)p.in_pitch | (uintptr_t)p.in_page_stride) &
+                      15u) == 0;
+    for (int idx = tid; idx < RH * nch; idx += kNT) {
+      const int ry = idx / nch, ch = idx - ry * nch;
+      const int64_t y = y0 + ry, x = xa + 16 * ch;
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (y >= 0 && y < p.H_global) {
+        const uint8_t* row = pg + (y - p.buf_row0) * p.in_pitch;
+        if (vec && x >= 0 && x + 16 <= p.W) {
+          v = __ldg(reinterpret_cast<const uint4*>(row + x));
+        } else {
+          uint32_t wv[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+          for (int b = 0; b < 16; ++b)
+            if (x + b >= 0 && x + b < p.W) wv[b >> 2] |= (uint32_t)__ldg(row + x + b) << (8 * (b & 3));
+          v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
       }
+      *reinterpret_cast<uint4*>(reg + ry * RWp + 16 * ch) = v;
     }
   }
   __syncthreads();
@@ -89,7 +104,7 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
     uint32_t c = 0, d = 0;
 #pragma unroll 4
     for (int y = 0; y < p.h; ++y) {
-      const uint32_t v = reg[y * RWp + x];
+      const uint32_t v = reg[y * RWp + dx + x];
       c += v;
       d += v * v;
     }
@@ -97,11 +112,11 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
     Ds[x] = d;
 #pragma unroll 4
     for (int t = 1; t < kTH; ++t) {
-      const uint32_t vi = reg[(t + p.h - 1) * RWp + x], vo = reg[(t - 1) * RWp + x];
+      const uint32_t vi = reg[(t + p.h - 1) * RWp + dx + x], vo = reg[(t - 1) * RWp + dx + x];
       c += vi - vo;
       d += vi * vi - vo * vo;
-      Cs[t * RWp + x] = c;
-      Ds[t * RWp + x] = d;
+      Cs[t * CWp + x] = c;
+      Ds[t * CWp + x] = d;
     }
   }
   __syncthreads();
@@ -110,8 +125,8 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
   const int64_t i = i0 + t;
   const int64_t jb = j0 + 16 * seg;
   if (i >= p.row0 + p.H_out || jb >= p.W) return;
-  const uint32_t* Cr = Cs + t * RWp + 16 * seg;
-  const uint32_t* Dr = Ds + t * RWp + 16 * seg;
+  const uint32_t* Cr = Cs + t * CWp + 16 * seg;
+  const uint32_t* Dr = Ds + t * CWp + 16 * seg;
   uint32_t c = 0, d = 0;
 #pragma unroll 4
   for (int x = 0; x < p.w; ++x) {
