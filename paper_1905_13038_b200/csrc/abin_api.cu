@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -142,7 +143,7 @@ int launch_v5_any(int w32, const CUtensorMap& map, const CUtensorMap& mpk, const
 }
 
 // resident v5 warp-CTAs per SM (registers and shared memory, as the runtime reports)
-int occupancy_v5_any(int w32, int method) {
+int occupancy_v5_query(int w32, int method) {
   switch (w32 >> 2) {
     case 0: return occupancy_v5_part0(w32, method);
     case 1: return occupancy_v5_part1(w32, method);
@@ -154,6 +155,28 @@ int occupancy_v5_any(int w32, int method) {
     case 7: return occupancy_v5_part7(w32, method);
   }
   return 16;
+}
+
+// resident v5 warp-CTAs per SM, cached per device, w mod 32 and method (the
+// runtime's occupancy query costs several microseconds of host time per call)
+int occupancy_v5_any(int w32, int method) {
+  static std::atomic<int> cache[64][32][16];
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (auto& a : cache)
+      for (auto& b : a)
+        for (auto& c : b) c.store(-1, std::memory_order_relaxed);
+  });
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || w32 < 0 || w32 >= 32 || method < 0 ||
+      method >= 16)
+    return occupancy_v5_query(w32, method);
+  int v = cache[dev][w32][method].load(std::memory_order_relaxed);
+  if (v < 0) {
+    v = occupancy_v5_query(w32, method);
+    cache[dev][w32][method].store(v, std::memory_order_relaxed);
+  }
+  return v;
 }
 
 int launch_wide_any(bool d64, bool stats, int nt, int ph, const CUtensorMap& map, const wide::MomParams& p,
@@ -325,8 +348,18 @@ int num_sms() {
 int warp_cta_slots(size_t dyn_smem) {
   int dev = 0, cap = 0, rsv = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 16;
+  static std::atomic<int> cap_c[64], rsv_c[64];  // per-device attributes (0: not read yet)
+  if (dev >= 0 && dev < 64 && cap_c[dev].load(std::memory_order_relaxed) > 0) {
+    cap = cap_c[dev].load(std::memory_order_relaxed);
+    rsv = rsv_c[dev].load(std::memory_order_relaxed);
+    return std::max(1, std::min(16, (int)(cap / (dyn_smem + (size_t)rsv))));
+  }
   if (cudaDeviceGetAttribute(&cap, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) != cudaSuccess) return 16;
   if (cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess) rsv = 1024;
+  if (dev >= 0 && dev < 64) {
+    rsv_c[dev].store(rsv, std::memory_order_relaxed);
+    cap_c[dev].store(cap, std::memory_order_relaxed);
+  }
   const int per = (int)(cap / (dyn_smem + (size_t)rsv));
   return std::max(1, std::min(16, per));
 }
