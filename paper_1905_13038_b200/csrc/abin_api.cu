@@ -647,7 +647,10 @@ int run_moments(const MomCall& c) {
   // path; the v3 kernel (inline exact path) for rules, statistics, forced fp64
   // and rows TMA cannot stage
   const bool d64_sq = (c.flags & ABIN_FORCE_U64_SQ) || (uint64_t)win.h * (uint64_t)win.w * 65025u >= (1ull << 32);
-  const bool v5_rule = rule && rule_on_v5(c.method, c.rprm, (double)win.h * (double)win.w) && !d64_sq &&
+  // (Feng and Rais: the v5 kernel with the double threshold for every pixel)
+  const bool v5_rule = rule &&
+                       (rule_on_v5(c.method, c.rprm, (double)win.h * (double)win.w) || c.method == ABIN_FENG ||
+                        c.method == ABIN_RAIS) && !d64_sq &&
                        win.h <= v5::kMaxH && win.w <= v5::kMaxW && !(c.flags & ABIN_V4_INTERNAL);
   const bool use_v4 = fast && tma_ok && !(c.flags & ABIN_V3_INTERNAL) && (!rule || v5_rule) && !stats &&
                       !(c.flags & ABIN_FORCE_FP64);

@@ -297,7 +297,13 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
   const int64_t Jend = min(J0 + (PACK ? (int64_t)kG * (G - KH) : (int64_t)p.Tw), p.W);
   const bool valid_lane = lane_ok && kl >= KH && j0 < Jend;
   const uint32_t vmask = valid_lane ? (Jend - j0 >= kG ? 0xFFFFu : ((1u << (uint32_t)(Jend - j0)) - 1u)) : 0u;
-  const float Lf = (METHOD == M_WOLF) ? (float)(p.L_fixed >= 0 ? p.L_fixed : (lane_ok ? (int)p.L_page[page] : 0)) : 0.0f;
+  const float Lf = (METHOD == M_WOLF || METHOD == M_FENG)
+                       ? (float)(p.L_fixed >= 0 ? p.L_fixed : (lane_ok ? (int)p.L_page[page] : 0)) : 0.0f;
+  // Feng and Rais (no certified fp32 bound): every pixel takes the rule's
+  // IEEE-double threshold in the epilogue (threshold_rule_fp64, the v3
+  // kernel's function), on the v5 kernel's exact window sums
+  constexpr bool kExact = METHOD == M_FENG || METHOD == M_RAIS;
+  unsigned long long x_near = 0, x_fp64 = 0;
   // Edge strips.  (1) -1/ncol per output column: ncol = w
   // except within (w+1)/2 columns of a border, so at most 10 lanes of a strip
   // see other counts; they get their own 16-entry slot of the table, every
@@ -574,6 +580,25 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
             (void)I;
             continue;
           }
+          if constexpr (kExact) {
+            // e = -1 (foreground, I <= t) or +1 per pixel, from the double threshold
+            const uint32_t nrow_x = (uint32_t)(min(i + p.u, p.H_global - 1) - max(i - p.o, (int64_t)-1));
+#pragma unroll
+            for (int z = 0; z < 2; ++z) {
+              const int64_t jx = j0 + t0 + z;
+              const uint32_t ncol_x = EDGE ? (uint32_t)(min(jx + p.r, p.W - 1) - max(jx - p.l, (int64_t)-1))
+                                           : (uint32_t)p.w;
+              const double tt = threshold_rule_fp64(METHOD, (uint64_t)(cq[z] - kBias), (uint64_t)dq[z],
+                                                    ncol_x * nrow_x, p.rp, (double)Lf, page);
+              const float Iz = z ? hi(I) : lo(I);
+              e4[h2 + z] = ((double)Iz <= tt) ? -1.0f : 1.0f;
+              if ((vmask >> (t0 + z)) & 1u) {
+                ++x_fp64;
+                if (fabs((double)Iz - tt) < 1e-9) ++x_near;
+              }
+            }
+            continue;
+          }
           f2 sv;
           const f2 e = residual_pair<METHOD>(cq[0], cq[1], dq[0], dq[1], nu, nb, I, fa2, fb2,
                                              aux_operand<METHOD>(p, Lf2, nu), sv, y2);
@@ -628,6 +653,18 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
       optr += out_pitch;
     }
     stage_end(s);
+  }
+  if constexpr (kExact) {
+    if (p.counters) {
+      for (int off = 16; off > 0; off >>= 1) {
+        x_near += __shfl_down_sync(0xffffffffu, x_near, off);
+        x_fp64 += __shfl_down_sync(0xffffffffu, x_fp64, off);
+      }
+      if (lane == 0) {
+        if (x_near) atomicAdd(reinterpret_cast<unsigned long long*>(&p.counters[0]), x_near);
+        if (x_fp64) atomicAdd(reinterpret_cast<unsigned long long*>(&p.counters[1]), x_fp64);
+      }
+    }
   }
   if (METHOD == M_MAXS && p.maxs_pass == 0) {
     // max v~ of the tile (>= 0: a clamp at 0 keeps the float bits ordered)

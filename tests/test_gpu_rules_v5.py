@@ -102,3 +102,43 @@ def test_rules_outside_v5_stay_exact():
     I = synth.page(60, 500, synth.config_seed(9, 2), stain=True)
     check("phansalkar", (0.25, 128.0, 3.0, -0.01), I, 9, 9)
     check("khurshid", (-0.1, 0), I, 9, 201)
+
+
+# ---- Feng and Rais on v5 with the double threshold for every pixel (no fp32 bound)
+EXACT_SETS = {"feng": [(0.12, 0.015, 0.01, 2.0, 128.0), (0.2, 0.05, 0.02, 1.5, 64.0)], "rais": [()]}
+
+
+@pytest.mark.parametrize("rule", sorted(EXACT_SETS))
+def test_feng_rais_on_v5(rule):
+    """Masks and near-tie counts equal the v3 kernel's (both evaluate the same
+    device double routine per pixel from exact sums) and the oracle's
+    (Rais: IEEE-exact operations, bit-exact; Feng's pow may differ from
+    glibc's in the last ulp: near ties excluded, R18), over every
+    w mod 32 class of the strip geometry, borders, bands of rows and batches."""
+    rng = np.random.default_rng(31)
+    for prm in EXACT_SETS[rule]:
+        for (H, W), (h, w) in [((130, 333), (15, 15)), ((200, 517), (61, 61)), ((77, 450), (40, 33)),
+                               ((150, 600), (129, 127)), ((40, 70), (9, 100)), ((96, 512), (4, 32))]:
+            I = synth.page(H, W, synth.config_seed(10, H + W), stain=True)
+            x = to_dev(I)
+            for packed in (False, True):
+                c5 = torch.zeros(2, dtype=torch.int64, device=DEV)
+                c3 = torch.zeros(2, dtype=torch.int64, device=DEV)
+                got = ab.binarize_rule(rule, x, h, w, prm, packed=packed, counters=c5).cpu().numpy()
+                v3 = ab.binarize_rule(rule, x, h, w, prm, packed=packed, counters=c3,
+                                      flags=abin.V3_INTERNAL).cpu().numpy()
+                assert np.array_equal(got, v3), (rule, prm, H, W, h, w, packed)
+                assert int(c5[0]) == int(c3[0])
+            ref, t = oracle.binarize_rule(rule, I, h, w, prm, with_t=True)
+            if rule == "rais":
+                assert np.array_equal(got if not packed else ab.binarize_rule(rule, x, h, w, prm).cpu().numpy(), ref)
+            else:
+                g = ab.binarize_rule(rule, x, h, w, prm).cpu().numpy()
+                tie = np.abs(I.astype(np.float64) - t) < 1e-9
+                assert not ((g != ref) & ~tie).any(), (rule, prm, h, w)
+        # random pixels (no structure): the rules' fractions and powers over the whole range
+        R = rng.integers(0, 256, size=(90, 300), dtype=np.uint8)
+        x = to_dev(R)
+        got = ab.binarize_rule(rule, x, 21, 37, prm).cpu().numpy()
+        v3 = ab.binarize_rule(rule, x, 21, 37, prm, flags=abin.V3_INTERNAL).cpu().numpy()
+        assert np.array_equal(got, v3), (rule, prm)
