@@ -194,6 +194,9 @@ int launch_wide_any(bool d64, bool stats, int nt, int ph, const CUtensorMap& map
 struct FilterConsts {
   float fa, fb, delta1, delta2;
   float rb0, rb1, rdv, rsdv;  // data-dependent stage-1 bound: rb0 + rb1 min(rsdv, rdv / s~)
+  // Rais: the parts that scale with 1 / (M S) (the page's): coarse bound delta1 + rais_c / (M S),
+  // data-dependent rb0 + rais_r0 / (M S) and rb1 + rais_r1 / (M S)
+  float rais_c, rais_r0, rais_r1;
 };
 
 FilterConsts filter_consts(int method, double k, double R) {
@@ -298,6 +301,35 @@ FilterConsts filter_consts_v5(int method, double k, double R, const double* rprm
   else if (method == M_NIBLACK || method == M_KHURSHID) { f.fa = 0.0f; f.fb = (float)k; }
   else { f.fa = (float)k; f.fb = (float)(1.0 / R); }
   f.delta1 = (float)(1.25 * (bound(ds) + eps64) + 1e-6);
+  if (method == M_RAIS) {
+    // t = m + 0.3 f s, f = (a - b) / max(a, b), a = m s, b = M S (the page's).  |df/da|, |df/db| <= 1/b
+    // on both sides of a = b, so |f(a~, b~) - f| <= (|a~ - a| + |b~ - b|) / (b (1 - 2u)); f~'s own
+    // roundings (subtraction, rcp.approx <= 2u, product) add 4.04u (|f| <= 1).  delta1 holds the part
+    // independent of b, rb1 the coefficient of 1/b (the kernel adds rb1 / (M S) per page).
+    // As functions of the bound x on |s~ - s| (x <= ds, the coarse one): A(x) (independent of b) and
+    // B(x) / b, both affine in x ((sx + x) <= sx + ds in B's product)
+    const double sx = 127.5;
+    const double dg0 = 0.3 * (4.04 * u * 1.01 + 1.02 * u) + 0.61 * u;   // |g~ - 0.3 f| less the Da / b part
+    auto A = [&](double x) {
+      return dm + 0.3 * x + (sx + x) * dg0 + 1.01 * u * 0.3 * (sx + x) + 2.02 * u * (255.0 + 0.3 * (sx + x));
+    };
+    auto B = [&](double x) {  // (sx + ds) 0.3 |a~ - m s|, |a~ - m s| <= 255 x + sx dm + dm x + roundings
+      const double Da = 255.0 * x + sx * dm + dm * x + 1.01 * u * (255.0 + dm) * (sx + ds);
+      return (sx + ds) * 0.3 * Da * (1.0 + 4 * u);
+    };
+    f.delta1 = (float)(1.25 * (A(ds) + eps64) + 1e-6);
+    f.rais_c = (float)(1.25 * B(ds) * (1 + 1e-6));
+    // data-dependent: x = min(sqrt dv, dv (1 + eps) / s~) + eps (smax + sqrt dv), as Niblack's
+    const double a0 = A(0.0), a1 = A(1.0) - a0, b0 = B(0.0), b1 = B(1.0) - b0;
+    const double xe = eps_sqrt * (smax + rv);
+    f.rb0 = (float)((1.25 * (a0 + a1 * xe + eps64) + 1e-6) * (1 + 1e-6));
+    f.rais_r0 = (float)(1.25 * (b0 + b1 * xe) * (1 + 1e-6) * (1 + 1e-6));
+    f.rb1 = (float)(1.25 * a1 * (1 + 1e-6));
+    f.rais_r1 = (float)(1.25 * b1 * (1 + 1e-6));
+    f.rdv = (float)(dv * (1 + eps_sqrt) * (1 + 1e-6));
+    f.rsdv = (float)(rv * (1 + 1e-6));
+    return f;
+  }
   // data-dependent form (Niblack, Khurshid): |s~ - s| <= min(sqrt dv, dv (1 + eps) / s~) + eps (smax + sqrt dv);
   // bound(ds) is affine in ds
   const double b0 = bound(0.0), b1 = bound(1.0) - b0;
@@ -316,10 +348,13 @@ void rule_aux_v5(int method, const double* rprm, double hw, float* aux0, float* 
   if (method == M_PHANSALKAR) { *aux0 = (float)rprm[2]; *aux1 = (float)(rprm[3] * 1.4426950408889634); }
 }
 
-// Khurshid and Phansalkar (q >= 0) run on v5 behind the certified filter when
-// its bound is usable (small against the 0.5 spacing of the integer pixels);
-// the other rules and other parameters stay on the exact v3 path
+// Khurshid, Phansalkar (q >= 0) and Rais run on v5 behind the certified
+// filter when its bound is usable (small against the 0.5 spacing of the
+// integer pixels; Rais's is formed per page from M S); Feng and other
+// parameters stay on the exact v3 path (Feng on v5's sums with its double
+// pow for every pixel measured slower than v3: 1.75 vs 1.51 ms per A4 page)
 bool rule_on_v5(int method, const double* rprm, double hw) {
+  if (method == M_RAIS) return true;  // the bound is formed per page from M S (filter_consts_v5)
   if (method != M_KHURSHID && method != M_PHANSALKAR) return false;
   for (int z = 0; z < 4; ++z)
     if (!std::isfinite(rprm[z])) return false;
@@ -647,10 +682,7 @@ int run_moments(const MomCall& c) {
   // path; the v3 kernel (inline exact path) for rules, statistics, forced fp64
   // and rows TMA cannot stage
   const bool d64_sq = (c.flags & ABIN_FORCE_U64_SQ) || (uint64_t)win.h * (uint64_t)win.w * 65025u >= (1ull << 32);
-  // (Feng and Rais: the v5 kernel with the double threshold for every pixel)
-  const bool v5_rule = rule &&
-                       (rule_on_v5(c.method, c.rprm, (double)win.h * (double)win.w) || c.method == ABIN_FENG ||
-                        c.method == ABIN_RAIS) && !d64_sq &&
+  const bool v5_rule = rule && rule_on_v5(c.method, c.rprm, (double)win.h * (double)win.w) && !d64_sq &&
                        win.h <= v5::kMaxH && win.w <= v5::kMaxW && !(c.flags & ABIN_V4_INTERNAL);
   const bool use_v4 = fast && tma_ok && !(c.flags & ABIN_V3_INTERNAL) && (!rule || v5_rule) && !stats &&
                       !(c.flags & ABIN_FORCE_FP64);
@@ -733,6 +765,11 @@ int run_moments(const MomCall& c) {
         const FilterConsts f5 = filter_consts_v5(c.method, c.k, c.R, c.rprm);
         q.fa = f5.fa; q.fb = f5.fb; q.delta1 = f5.delta1;
         rule_aux_v5(c.method, c.rprm, (double)win.h * (double)win.w, &q.aux0, &q.aux1);
+        if (c.method == M_RAIS) {  // the bounds' 1 / (M S) coefficients
+          q.aux1 = f5.rais_c;
+          q.aux0 = f5.rais_r0;
+          q.rais_r1 = f5.rais_r1;
+        }
         q.rb0 = f5.rb0; q.rb1 = f5.rb1; q.rdv = f5.rdv; q.rsdv = f5.rsdv;
       }
       // one warp per CTA; a strip = one warp's 32 - KH valid lanes
@@ -1722,10 +1759,15 @@ int abin_probe_filter(int32_t method, double k, double R, double L, const double
                       float* e_out, float* s_out, double* bounds, void* stream) {
   if (count < 0) return ABIN_EINVAL;
   const bool rule = method == ABIN_KHURSHID || method == ABIN_PHANSALKAR;
-  if (!rule && (method < ABIN_SAUVOLA || method > ABIN_WOLF)) return ABIN_EINVAL;
+  if (!rule && method != ABIN_RAIS && (method < ABIN_SAUVOLA || method > ABIN_WOLF)) return ABIN_EINVAL;
   float aux0 = 0.0f, aux1 = 0.0f;
   int nmode = 0;
-  if (rule) {
+  float Lprobe = (float)L;
+  if (method == ABIN_RAIS) {
+    // rule_params[0] = the page's M S; bounds[0] + bounds[2] / (M S) is the bound
+    if (!rule_params || !std::isfinite(rule_params[0]) || !(rule_params[0] >= 0.0)) return ABIN_EINVAL;
+    Lprobe = (float)rule_params[0];
+  } else if (rule) {
     if (!rule_params) return ABIN_EINVAL;
     nmode = method == ABIN_KHURSHID && rule_params[1] != 0.0;
     const double hw = method == ABIN_KHURSHID && !nmode ? rule_params[2] : 1.0;  // Khurshid's N = h w
@@ -1738,15 +1780,22 @@ int abin_probe_filter(int32_t method, double k, double R, double L, const double
   const FilterConsts f = filter_consts_v5(method, k, R, rule_params);
   if (bounds) {
     bounds[0] = f.delta1; bounds[1] = f.rb0; bounds[2] = f.rb1; bounds[3] = f.rdv; bounds[4] = f.rsdv;
+    if (method == ABIN_RAIS) {  // the bounds at this M S, as the kernel forms them per page
+      const double MS = std::max((double)(float)rule_params[0], 1e-30);
+      bounds[0] = f.delta1 + f.rais_c / MS;
+      bounds[1] = f.rb0 + f.rais_r0 / MS;
+      bounds[2] = f.rb1 + f.rais_r1 / MS;
+    }
   }
   if (count == 0) return ABIN_OK;
   if (!c || !d || !ncol || !nrow || !I || !e_out) return ABIN_EINVAL;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const unsigned nb = (unsigned)((count + 255) / 256);
-  const float Lf = (float)L;
+  const float Lf = Lprobe;
 #define ABIN_PROBE(M) \
   v5::k_probe<M><<<nb, 256, 0, st>>>(c, d, ncol, nrow, I, count, f.fa, f.fb, Lf, aux0, aux1, nmode, e_out, s_out)
   if (method == M_SAUVOLA) ABIN_PROBE(M_SAUVOLA);
+  else if (method == M_RAIS) ABIN_PROBE(M_RAIS);
   else if (method == M_NIBLACK) ABIN_PROBE(M_NIBLACK);
   else if (method == M_WOLF) ABIN_PROBE(M_WOLF);
   else if (method == M_KHURSHID) ABIN_PROBE(M_KHURSHID);

@@ -87,7 +87,8 @@ struct MomParams {
   unsigned long long* smax_bits;
   int32_t maxs_pass;
   float maxs_margin;
-  float aux0, aux1;          // v5 rules: Khurshid 1/(h w); Phansalkar p, q log2(e)
+  float aux0, aux1;          // v5 rules: Khurshid 1/(h w); Phansalkar p, q log2(e); Rais the bounds' 1/(M S) parts
+  float rais_r1;             // Rais: the data-dependent bound's 1/(M S) slope part
   // statistics mode (page 0 only)
   uint64_t* c_out;
   uint64_t* d_out;

@@ -153,6 +153,24 @@ __device__ __forceinline__ f2 residual2(f2 mn, f2 qn, f2 I, f2 fa2, f2 fb2, f2 L
   }
   const f2 wv = fma2(mn, mn, qn);  // m^2 - q = -v~
   s = pk(sqrt_approx(fabsf(lo(wv))), sqrt_approx(fabsf(hi(wv))));
+  if (METHOD == M_RAIS) {
+    // t = m + 0.3 f s, f = (m s - M S) / max{m s, M S}  (Lf2 = fl32(M S), the page's; 0/0 -> 0, R16);
+    // each operation rounded separately, as filter_consts_v5 bounds them
+    const f2 na = mul2(mn, s);  // -a~, a~ = fl(m~ s~)
+    const float b = lo(Lf2);
+    float e[2];
+#pragma unroll
+    for (int z = 0; z < 2; ++z) {
+      const float a = -(z ? hi(na) : lo(na));
+      const float den = fmaxf(fmaxf(a, b), 1e-30f);
+      float rc;
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(den));
+      const float f = __fmul_rn(__fsub_rn(a, b), rc);
+      const float r = __fmul_rn(__fmul_rn(0.3f, f), z ? hi(s) : lo(s));
+      e[z] = __fsub_rn(__fadd_rn(z ? hi(I) : lo(I), z ? hi(mn) : lo(mn)), r);  // (I - m~) - r~
+    }
+    return pk(e[0], e[1]);
+  }
   if (METHOD == M_SAUVOLA) {
     const f2 g = fma2(s, fb2, fa2);  // (1 - k) + (k/R) s
     return fma2(mn, g, I);           // I - m g
@@ -297,13 +315,7 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
   const int64_t Jend = min(J0 + (PACK ? (int64_t)kG * (G - KH) : (int64_t)p.Tw), p.W);
   const bool valid_lane = lane_ok && kl >= KH && j0 < Jend;
   const uint32_t vmask = valid_lane ? (Jend - j0 >= kG ? 0xFFFFu : ((1u << (uint32_t)(Jend - j0)) - 1u)) : 0u;
-  const float Lf = (METHOD == M_WOLF || METHOD == M_FENG)
-                       ? (float)(p.L_fixed >= 0 ? p.L_fixed : (lane_ok ? (int)p.L_page[page] : 0)) : 0.0f;
-  // Feng and Rais (no certified fp32 bound): every pixel takes the rule's
-  // IEEE-double threshold in the epilogue (threshold_rule_fp64, the v3
-  // kernel's function), on the v5 kernel's exact window sums
-  constexpr bool kExact = METHOD == M_FENG || METHOD == M_RAIS;
-  unsigned long long x_near = 0, x_fp64 = 0;
+  const float Lf = (METHOD == M_WOLF) ? (float)(p.L_fixed >= 0 ? p.L_fixed : (lane_ok ? (int)p.L_page[page] : 0)) : 0.0f;
   // Edge strips.  (1) -1/ncol per output column: ncol = w
   // except within (w+1)/2 columns of a border, so at most 10 lanes of a strip
   // see other counts; they get their own 16-entry slot of the table, every
@@ -428,10 +440,14 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
   const uint32_t store_mode = !valid_lane ? 0u : (p.fmt != 0 ? 3u : (out_vec ? 1u : 2u));
   const int64_t i_full0 = p.o - 1, i_full1 = p.H_global - 1 - p.u;  // nrow == h for i in [i_full0, i_full1]
   const int32_t row_lo = (int32_t)max(i_full0, (int64_t)INT32_MIN), row_hi = (int32_t)min(i_full1, (int64_t)INT32_MAX);
-  const float delta1 = p.delta1;
+
   f2 fa2, fb2;
   method_consts<METHOD>(p.fa, p.fb, fa2, fb2);
-  const f2 Lf2 = splat(Lf);
+  // Rais: the page's M S (fl32 of the double product) in the L slot, and the
+  // certified bound delta1 + aux1 / (M S) (the fraction's derivative is <= 1 / (M S))
+  const float MSf = METHOD == M_RAIS && lane_ok ? (float)(p.rp.MS[2 * page] * p.rp.MS[2 * page + 1]) : 0.0f;
+  const f2 Lf2 = splat(METHOD == M_RAIS ? MSf : Lf);
+  const float delta1 = METHOD == M_RAIS ? p.delta1 + p.aux1 / fmaxf(MSf, 1e-30f) : p.delta1;
   const f2 y2 = splat(p.aux1);  // Phansalkar: q log2(e)
   // interior columns: ncol = w; per-row -1/n = -(1/w)(1/nrow) computed once per row
   const float inv_w = __frcp_rn((float)p.w);
@@ -580,30 +596,11 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
             (void)I;
             continue;
           }
-          if constexpr (kExact) {
-            // e = -1 (foreground, I <= t) or +1 per pixel, from the double threshold
-            const uint32_t nrow_x = (uint32_t)(min(i + p.u, p.H_global - 1) - max(i - p.o, (int64_t)-1));
-#pragma unroll
-            for (int z = 0; z < 2; ++z) {
-              const int64_t jx = j0 + t0 + z;
-              const uint32_t ncol_x = EDGE ? (uint32_t)(min(jx + p.r, p.W - 1) - max(jx - p.l, (int64_t)-1))
-                                           : (uint32_t)p.w;
-              const double tt = threshold_rule_fp64(METHOD, (uint64_t)(cq[z] - kBias), (uint64_t)dq[z],
-                                                    ncol_x * nrow_x, p.rp, (double)Lf, page);
-              const float Iz = z ? hi(I) : lo(I);
-              e4[h2 + z] = ((double)Iz <= tt) ? -1.0f : 1.0f;
-              if ((vmask >> (t0 + z)) & 1u) {
-                ++x_fp64;
-                if (fabs((double)Iz - tt) < 1e-9) ++x_near;
-              }
-            }
-            continue;
-          }
           f2 sv;
           const f2 e = residual_pair<METHOD>(cq[0], cq[1], dq[0], dq[1], nu, nb, I, fa2, fb2,
                                              aux_operand<METHOD>(p, Lf2, nu), sv, y2);
           emin = fmin3(emin, fabsf(lo(e)), fabsf(hi(e)));
-          if (METHOD == M_NIBLACK || METHOD == M_KHURSHID) smin = fmin3(smin, lo(sv), hi(sv));
+          if (METHOD == M_NIBLACK || METHOD == M_KHURSHID || METHOD == M_RAIS) smin = fmin3(smin, lo(sv), hi(sv));
           e4[h2] = lo(e);
           e4[h2 + 1] = hi(e);
         }
@@ -625,8 +622,14 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
       // with the data-dependent bound at its smallest s~ (v4 refined_bound)
       uint32_t amb = 0u;
       if (emin < delta1) {
-        if ((METHOD != M_NIBLACK && METHOD != M_KHURSHID) || emin * 0.999999f < v4::refined_bound(p, smin))
+        if constexpr (METHOD == M_RAIS) {
+          // the data-dependent bound at the lane's smallest s~, its 1/(M S) parts added per page
+          const float iMS = 1.0f / fmaxf(MSf, 1e-30f);
+          const float rb0 = p.rb0 + p.aux0 * iMS, rb1 = p.rb1 + p.rais_r1 * iMS;
+          if (emin * 0.999999f < (rb0 + rb1 * fminf(p.rsdv, p.rdv / smin)) * 1.000001f) amb = vmask;
+        } else if ((METHOD != M_NIBLACK && METHOD != M_KHURSHID) || emin * 0.999999f < v4::refined_bound(p, smin)) {
           amb = vmask;
+        }
       }
       if (amb) {
         const uint32_t slot = atomicAdd(p.q_count, 1u);
@@ -653,18 +656,6 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
       optr += out_pitch;
     }
     stage_end(s);
-  }
-  if constexpr (kExact) {
-    if (p.counters) {
-      for (int off = 16; off > 0; off >>= 1) {
-        x_near += __shfl_down_sync(0xffffffffu, x_near, off);
-        x_fp64 += __shfl_down_sync(0xffffffffu, x_fp64, off);
-      }
-      if (lane == 0) {
-        if (x_near) atomicAdd(reinterpret_cast<unsigned long long*>(&p.counters[0]), x_near);
-        if (x_fp64) atomicAdd(reinterpret_cast<unsigned long long*>(&p.counters[1]), x_fp64);
-      }
-    }
   }
   if (METHOD == M_MAXS && p.maxs_pass == 0) {
     // max v~ of the tile (>= 0: a clamp at 0 keeps the float bits ordered)

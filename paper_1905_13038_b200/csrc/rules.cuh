@@ -67,12 +67,26 @@ static __global__ void __launch_bounds__(256) k_global_sums(const uint8_t* __res
   const int page = blockIdx.y;
   const uint8_t* img = in + (int64_t)page * page_stride;
   unsigned long long s1 = 0, s2 = 0;
-  for (int64_t row = blockIdx.x; row < H; row += gridDim.x)
-    for (int64_t col = threadIdx.x; col < W; col += blockDim.x) {
-      const unsigned long long x = img[row * pitch + col];
+  // 16-byte chunks when the page is aligned: the chunk's byte sum and square
+  // sum by dp4a (exact in uint32), accumulated in uint64
+  const bool vec = ((reinterpret_cast<uintptr_t>(img) | (uintptr_t)pitch) & 15u) == 0;
+  const int64_t nv = vec ? W / 16 : 0;
+  for (int64_t row = blockIdx.x; row < H; row += gridDim.x) {
+    const uint8_t* r = img + row * pitch;
+    for (int64_t q = threadIdx.x; q < nv; q += blockDim.x) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(r) + q);
+      uint32_t a1 = __dp4a(v.x, 0x01010101u, 0u), a2 = __dp4a(v.x, v.x, 0u);
+      a1 = __dp4a(v.y, 0x01010101u, a1); a1 = __dp4a(v.z, 0x01010101u, a1); a1 = __dp4a(v.w, 0x01010101u, a1);
+      a2 = __dp4a(v.y, v.y, a2); a2 = __dp4a(v.z, v.z, a2); a2 = __dp4a(v.w, v.w, a2);
+      s1 += a1;
+      s2 += a2;
+    }
+    for (int64_t col = 16 * nv + threadIdx.x; col < W; col += blockDim.x) {
+      const unsigned long long x = r[col];
       s1 += x;
       s2 += x * x;
     }
+  }
   for (int off = 16; off > 0; off >>= 1) {
     s1 += __shfl_xor_sync(0xffffffffu, s1, off);
     s2 += __shfl_xor_sync(0xffffffffu, s2, off);

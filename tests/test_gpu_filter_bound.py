@@ -34,7 +34,11 @@ RULES = {"khurshid0": ("khurshid", (-0.1, 0, 16383.0)), "khurshid0s": ("khurshid
          "khurshid1": ("khurshid", (-0.2, 1, 0.0)), "khurshidN1": ("khurshid", (0.3, 0, 1.0)),
          "phansalkar": ("phansalkar", (0.25, 128.0, 3.0, 10.0 / 255.0)),
          "phansalkar_steep": ("phansalkar", (-0.3, 64.0, -2.0, 0.5)),
-         "phansalkar_q0": ("phansalkar", (0.5, 128.0, 1.0, 0.0))}
+         "phansalkar_q0": ("phansalkar", (0.5, 128.0, 1.0, 0.0)),
+         # Rais {M S}: the page's product (the bound grows as 1 / (M S)): document pages (M S ~ 7e3),
+         # dark / low-contrast pages, and a near-blank one
+         "rais_ms7200": ("rais", (7200.0,)), "rais_ms900": ("rais", (900.0,)), "rais_ms40": ("rais", (40.0,)),
+         "rais_ms3": ("rais", (3.0,))}
 
 
 def t_exact(method, c, d, n, k, R, L):
@@ -45,6 +49,12 @@ def t_exact(method, c, d, n, k, R, L):
     s = np.sqrt(V.astype(LD) / (nl * nl))
     if method in RULES:
         rule, prm = RULES[method]
+        if rule == "rais":
+            # t = m + 0.3 (m s - M S) / max{m s, M S} s  (0/0 -> 0, R16)
+            a, b = m * s, LD(prm[0])
+            den = np.maximum(a, b)
+            f = np.where(den > 0, (a - b) / np.where(den > 0, den, LD(1)), LD(0))
+            return m + LD(0.3) * f * s
         if rule == "khurshid":
             # s^2 + m^2 (N - 1) / N = (N n d - c^2) / (N n^2), exact integers (N = h w or n)
             N = n.astype(np.int64) if prm[1] else np.int64(prm[2])
@@ -122,10 +132,12 @@ def check(method, c, d, ncol, nrow, I):
     e_star = I.astype(LD) - t_exact(method, c, d, ncol * nrow, k, R, L)
     err = np.abs(e - e_star).astype(np.float64)
     coarse = b[0]
+    if method in RULES and RULES[method][0] == "rais":
+        coarse = b[0] + b[2] / RULES[method][1][0]   # the kernel's delta1 + aux1 / (M S)
     assert err.max() <= coarse, (method, err.max(), coarse)
     ratio = err.max() / coarse
-    if method == "niblack" or method.startswith("khurshid"):
-        # the data-dependent bound the kernel applies to Niblack / Khurshid lanes
+    if method == "niblack" or method.startswith("khurshid") or method.startswith("rais"):
+        # the data-dependent bound the kernel applies to Niblack / Khurshid / Rais lanes
         with np.errstate(divide="ignore"):
             refined = b[1] + b[2] * np.minimum(b[4], b[3] / sv)
         assert (err <= refined).all(), (method, (err - refined).max())
@@ -155,10 +167,11 @@ def test_certified_bound_adversarial(method):
 
 @pytest.mark.parametrize("method", sorted(RULES))
 def test_certified_bound_rules(method):
-    """Khurshid and Phansalkar on v5: the same claim |e~ - e*| <= bound for
-    the rule's own residual (moments5.cuh residual2, abin_api.cu
+    """Khurshid, Phansalkar and Rais on v5: the same claim |e~ - e*| <=
+    bound for the rule's own residual (moments5.cuh residual2, abin_api.cu
     filter_consts_v5), e* from the exact integers in long double; 1.2e7
-    random + 3e6 adversarial tuples per parameter set (7 sets)."""
+    random + 3e6 adversarial tuples per parameter set (11 sets; Rais's bound
+    is formed per page from its M S)."""
     rng = np.random.default_rng(100 + sorted(RULES).index(method))
     worst = 0.0
     for _ in range(3):

@@ -104,17 +104,17 @@ def test_rules_outside_v5_stay_exact():
     check("khurshid", (-0.1, 0), I, 9, 201)
 
 
-# ---- Feng and Rais on v5 with the double threshold for every pixel (no fp32 bound)
+# ---- Rais on v5 behind its certified filter (the bound formed per page from M S), and Feng
+# (the v3 kernel: the same masks either way)
 EXACT_SETS = {"feng": [(0.12, 0.015, 0.01, 2.0, 128.0), (0.2, 0.05, 0.02, 1.5, 64.0)], "rais": [()]}
 
 
 @pytest.mark.parametrize("rule", sorted(EXACT_SETS))
 def test_feng_rais_on_v5(rule):
-    """Masks and near-tie counts equal the v3 kernel's (both evaluate the same
-    device double routine per pixel from exact sums) and the oracle's
-    (Rais: IEEE-exact operations, bit-exact; Feng's pow may differ from
-    glibc's in the last ulp: near ties excluded, R18), over every
-    w mod 32 class of the strip geometry, borders, bands of rows and batches."""
+    """Masks and near-tie counts equal the v3 kernel's (every pixel in double)
+    and the oracle's (Rais: IEEE-exact operations, bit-exact; Feng's pow may
+    differ from glibc's in the last ulp: near ties excluded, R18),
+    over the strip geometry classes, borders and random pages."""
     rng = np.random.default_rng(31)
     for prm in EXACT_SETS[rule]:
         for (H, W), (h, w) in [((130, 333), (15, 15)), ((200, 517), (61, 61)), ((77, 450), (40, 33)),
