@@ -137,9 +137,38 @@ static __device__ __noinline__ uint32_t exact_decide(const Q5Params& p, int page
   const int64_t r0 = max(i - p.o + 1, lo_row), r1 = min(i + p.u, hi_row - 1);
   const int64_t cl = max(j - p.l + 1, (int64_t)0), cr = min(j + p.r, p.W - 1);
   uint32_t cnt = 0;
-  for (int64_t g = r0 + lane; g <= r1; g += 32) {
-    const uint8_t* row = img + (g - p.buf_row0) * p.in_pitch;
-    for (int64_t c = cl; c <= cr; ++c) cnt += (int)__ldg(row + c) < I ? 1u : 0u;
+  if (((reinterpret_cast<uintptr_t>(img) | (uintptr_t)p.in_pitch) & 15u) == 0) {
+    // 16-byte chunks: lane = (chunk lane & 7 of the window's columns, row offset lane >> 3);
+    // bytes below I by a SIMD compare, bytes outside [cl, cr] masked (rows are 16-aligned and
+    // their last partial chunk readable: abin.h)
+    const int64_t ca = cl & ~(int64_t)15;
+    const int nch = (int)((cr - ca) / 16 + 1);
+    const uint32_t Iw = (uint32_t)I * 0x01010101u;
+    for (int k = lane & 7; k < nch; k += 8) {
+      const int64_t x0 = ca + 16 * k;
+      uint32_t vm[4];
+#pragma unroll
+      for (int wq = 0; wq < 4; ++wq) {
+        uint32_t m = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int64_t x = x0 + 4 * wq + b;
+          if (x >= cl && x <= cr) m |= 0xFFu << (8 * b);
+        }
+        vm[wq] = m;
+      }
+      for (int64_t g = r0 + (lane >> 3); g <= r1; g += 4) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(img + (g - p.buf_row0) * p.in_pitch + x0));
+        cnt += __popc(__vcmpltu4(v.x, Iw) & vm[0]) + __popc(__vcmpltu4(v.y, Iw) & vm[1]) +
+               __popc(__vcmpltu4(v.z, Iw) & vm[2]) + __popc(__vcmpltu4(v.w, Iw) & vm[3]);
+      }
+    }
+    cnt >>= 3;  // 8 bits per byte below I
+  } else {
+    for (int64_t g = r0 + lane; g <= r1; g += 32) {
+      const uint8_t* row = img + (g - p.buf_row0) * p.in_pitch;
+      for (int64_t c = cl; c <= cr; ++c) cnt += (int)__ldg(row + c) < I ? 1u : 0u;
+    }
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
