@@ -65,6 +65,25 @@ struct Window {
   int32_t h, w, l, r, o, u;
 };
 
+// Experiment and test hooks: read on every call and
+// parsed / clamped in one place; unset (or "0" for the flags) means the
+// measured defaults.
+bool env_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && *e && strcmp(e, "0") != 0;
+}
+long long env_int(const char* name, long long def, long long lo, long long hi) {
+  const char* e = getenv(name);
+  if (!e || !*e) return def;
+  return std::max(lo, std::min(hi, atoll(e)));
+}
+double env_real(const char* name, double def, double lo, double hi) {
+  const char* e = getenv(name);
+  if (!e || !*e) return def;
+  const double v = atof(e);
+  return std::isfinite(v) ? std::max(lo, std::min(hi, v)) : def;
+}
+
 // Alg. 1 l.1-4, then clamp the reach to the image: replacing
 // l by min(l, W) (etc.) changes neither the in-bounds window nor n.
 Window effective_window(int32_t h, int32_t w, int64_t Hg, int64_t W) {
@@ -473,8 +492,7 @@ void choose_bands_v4(int64_t col_tiles, int64_t H_out, int32_t h, int slots, int
   // 255), 0.5 for small batches and wide pages (16 config-3 pages, config 4),
   // 0.8 for large batches, whose many waves make warm-up rows count more than
   // the tail (64 config-3 pages: 699 -> 714 Gpx/s)
-  static const char* wu_env = getenv("ABIN_V4_WU");
-  const double wu = wu_env ? atof(wu_env) : (col_tiles < 32 ? 0.3 : (col_tiles >= 512 ? 0.8 : 0.5));
+  const double wu = env_real("ABIN_V4_WU", col_tiles < 32 ? 0.3 : (col_tiles >= 512 ? 0.8 : 0.5), 0.0, 8.0);
   for (int64_t nb = 1; nb <= nb_max; ++nb) {
     const int64_t Bc = (H_out + nb - 1) / nb;
     const int64_t tiles = col_tiles * ((H_out + Bc - 1) / Bc);
@@ -568,8 +586,7 @@ int run_small(const MomCall& c, const Window& win) {
   const bool stats = c.c_out || c.d_out || c.n_out || c.t_out || c.mask_out;
   const uint32_t forced = ABIN_FORCE_FP64 | ABIN_FORCE_U64_SQ | ABIN_V3_INTERNAL | ABIN_V4_INTERNAL |
                           ABIN_NO_TMA_INTERNAL;
-  const char* px_env = getenv("ABIN_SMALL_PX");  // tests / experiments: the size limit (0: off)
-  const int64_t max_px = px_env ? atoll(px_env) : (int64_t)1 << 19;
+  const int64_t max_px = env_int("ABIN_SMALL_PX", 1ll << 19, 0, 1ll << 40);  // tests / experiments (0: off)
   if (stats || (c.flags & forced) || win.h > kMaxWin || win.w > kMaxWin ||
       !(c.method == M_SAUVOLA || c.method == M_NIBLACK || c.method == M_WOLF) ||
       c.n_pages * c.H_out * c.W > max_px)
@@ -787,7 +804,7 @@ int run_moments(const MomCall& c) {
       // strips of NG pages share one warp -- G = KH + its output lanes each,
       // one TMA box of NG pages -- instead of a mostly idle warp per page
       CUtensorMap mpk = map4;
-      if (use_v5 && c.method != M_MAXS && c.n_pages >= 2 && q.n_strips >= 2 && !getenv("ABIN_NO_PACK")) {
+      if (use_v5 && c.method != M_MAXS && c.n_pages >= 2 && q.n_strips >= 2 && !env_flag("ABIN_NO_PACK")) {
         const int64_t rem = c.W - (int64_t)(q.n_strips - 1) * q.Tw;  // outputs of the last strip
         const int G = q.KH + (int)((rem + kG - 1) / kG);
         const int NG = std::min(32 / G, v5::kRowsBytes / (v5::kR * kG * (G + 1)));
@@ -805,8 +822,8 @@ int run_moments(const MomCall& c) {
       choose_bands_v4(col_tiles, c.H_out, win.h,
                       num_sms() * (use_v5 ? occupancy_v5_any(win.w % 32, c.method) : warp_cta_slots(v4::smem_bytes())),
                       &q.B, &q.n_bands);
-      if (const char* nb = getenv("ABIN_V4_BANDS")) {  // experiments: force the band count
-        const int64_t want = std::max<int64_t>(1, std::min<int64_t>(atoll(nb), c.H_out));
+      if (const long long want_nb = env_int("ABIN_V4_BANDS", 0, 0, c.H_out)) {  // experiments: force the band count
+        const int64_t want = std::max<int64_t>(1, want_nb);
         q.B = (int32_t)((c.H_out + want - 1) / want);
         q.n_bands = (int32_t)((c.H_out + q.B - 1) / q.B);
       }
@@ -815,8 +832,8 @@ int run_moments(const MomCall& c) {
       // overflow, so they need no follow-up launch and a smaller queue
       const int64_t max_entries = c.n_pages * c.H_out * ((c.W + 15) / 16 + q.n_strips + 1);
       uint32_t cap = (uint32_t)std::min<int64_t>(1 << 22, max_entries);  // <= 64 MB: one A4 page at 600 dpi fits
-      if (const char* qc = getenv("ABIN_QUEUE_CAP"))  // tests: exercise the overflow follow-up
-        cap = (uint32_t)std::max<long long>(1, std::min<long long>(atoll(qc), 1ll << 26));
+      if (env_int("ABIN_QUEUE_CAP", 0, 0, 1ll << 26) > 0)  // tests: exercise the overflow follow-up
+        cap = (uint32_t)env_int("ABIN_QUEUE_CAP", 0, 1, 1ll << 26);
       const bool may_overflow = max_entries > (int64_t)cap;
       CK(cudaMallocAsync(&queue, (size_t)cap * 16 + 16, c.stream));
       uint32_t* qcount = reinterpret_cast<uint32_t*>(queue + (size_t)cap);
@@ -1016,14 +1033,13 @@ int run_quant5(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64
   // strokes' or the background's (three windows placed at q/2, q, 2q of the
   // tile sample).  ABIN_Q5_NW overrides (experiments).
   int nw = q >= 0.2 ? 1 : 3;
-  if (const char* e = getenv("ABIN_Q5_NW")) nw = std::max(1, std::min(q5::kMaxNW, atoi(e)));
+  nw = (int)env_int("ABIN_Q5_NW", nw, 1, q5::kMaxNW);
   p.nw = nw;
   const float qf = (float)q;
   if (nw == 1) { p.qf[0] = qf; }
   else if (nw == 2) { p.qf[0] = 0.5f * qf; p.qf[1] = std::min(1.0f, 2.0f * qf); }
   else { p.qf[0] = 0.5f * qf; p.qf[1] = qf; p.qf[2] = std::min(1.0f, 2.0f * qf); }
-  p.force_L = -1;
-  if (const char* e = getenv("ABIN_Q5_FORCE_L")) p.force_L = std::max(0, std::min(240, atoi(e)));  // tests
+  p.force_L = (int32_t)env_int("ABIN_Q5_FORCE_L", -1, 0, 240);  // tests (unset: -1, the sample's placement)
   const int wr = win.w % 16;
   int occ = 0;
   int rc = launch_q5_any(wr, p, 0, st, &occ);
@@ -1033,8 +1049,7 @@ int run_quant5(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64
     // the h warm-up rows (column adds only: about a fifth of a row each) and
     // its set-up (sample histogram, tables: about four rows)
     const int64_t cols = (int64_t)p.n_strips * n_pages, slots = (int64_t)num_sms() * std::max(1, occ);
-    static const char* wu_env = getenv("ABIN_Q5_WU");  // experiments: warm-up row weight
-    const double wu = wu_env ? atof(wu_env) : 0.2;
+    const double wu = env_real("ABIN_Q5_WU", 0.2, 0.0, 8.0);  // experiments: warm-up row weight
     double best = 1e300;
     int64_t bestB = H_out;
     for (int64_t nb = 1; nb <= std::max<int64_t>(1, H_out / 4); ++nb) {
@@ -1044,8 +1059,8 @@ int run_quant5(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64
       if (cost < best * 0.999) { best = cost; bestB = Bc; }
       if (cols * nb > 64 * slots) break;
     }
-    if (const char* nb = getenv("ABIN_Q5_BANDS")) {  // experiments: force the band count
-      const int64_t want = std::max<int64_t>(1, std::min<int64_t>(atoll(nb), H_out));
+    if (const long long want_nb = env_int("ABIN_Q5_BANDS", 0, 0, H_out)) {  // experiments: force the band count
+      const int64_t want = std::max<int64_t>(1, want_nb);
       bestB = (H_out + want - 1) / want;
     }
     p.B = (int32_t)bestB;
@@ -1054,7 +1069,7 @@ int run_quant5(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64
   // the exact queue: 16 bytes per undecided pixel; a full queue is decided inline
   const int64_t px = n_pages * H_out * W;
   uint32_t cap = (uint32_t)std::min<int64_t>(px, 1 << 20);
-  if (const char* e = getenv("ABIN_Q5_QCAP")) cap = (uint32_t)std::max<long long>(1, std::min<long long>(atoll(e), cap));
+  cap = (uint32_t)env_int("ABIN_Q5_QCAP", cap, 1, cap);  // tests: a full queue decides inline
   uint4* queue = nullptr;
   CK(cudaMallocAsync(&queue, (size_t)cap * 16 + 16, st));
   uint32_t* qcount = reinterpret_cast<uint32_t*>(queue + cap);
@@ -1062,7 +1077,7 @@ int run_quant5(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int64
   p.fq = queue; p.fq_count = qcount; p.fq_cap = cap;
   p.counters = reinterpret_cast<unsigned long long*>(counters);
   const int64_t n_tiles = (int64_t)p.n_strips * p.n_bands * n_pages;
-  if (getenv("ABIN_DEBUG"))
+  if (env_flag("ABIN_DEBUG"))
     fprintf(stderr, "q5: w %d h %d nw %d strips %d bands %d B %d occ %d tiles %lld\n", win.w, win.h, nw, p.n_strips,
             p.n_bands, p.B, occ, (long long)n_tiles);
   rc = launch_q5_any(wr, p, n_tiles, st, nullptr);
@@ -1124,7 +1139,7 @@ int run_bernsen(const uint8_t* in, int64_t in_page_stride, int64_t n_pages, int6
   p.sbs = (win.h + R - 1) / R;
   R = (win.h + p.sbs - 1) / p.sbs;
   const size_t vsm_need = (size_t)R * 32 * p.sbs * 16;
-  const bool v_smem = vsm_need <= 96 * 1024 && !getenv("ABIN_BERN_GSB");  // (experiments: global sb)
+  const bool v_smem = vsm_need <= 96 * 1024 && !env_flag("ABIN_BERN_GSB");  // (experiments: global sb)
   const size_t vsm = v_smem ? vsm_need : 0;
   void* scratch = nullptr;
   const size_t hb_bytes = (size_t)n_pages * p.Yn * p.hpitch * 2;
@@ -1170,7 +1185,7 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
   // 16-level windows per tile do not cover (measured: 1-35 % of the pixels to
   // the exact queue at q = 0.1), so they keep the round-1 kernels.
   // ABIN_Q5_ALWAYS (tests) takes v5 for every q.
-  const bool q5_always = getenv("ABIN_Q5_ALWAYS") != nullptr;
+  const bool q5_always = env_flag("ABIN_Q5_ALWAYS");
   if (method == ABIN_QUANTILE && !Q_out && !(flags & ABIN_Q2_INTERNAL) && (q >= 0.2 || q5_always)) {
     const int rc = run_quant5(in, in_page_stride, n_pages, W, in_pitch, out, out_pitch, out_page_stride, fmt, win, q,
                               row0, H_out, H_global, buf_rows, buf_row0, st, counters);
@@ -1207,7 +1222,7 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
   // byte deltas 128 + Delta with |Delta| <= h + 2 transiently)
   const bool pair = (method == ABIN_QUANTILE || method == ABIN_BERNSEN) && win.h <= 125 && 2 * NT2 + win.w <= 4 * NT2 &&
                     (int64_t)(win.h + 1) * win.w <= 65535 &&
-                    !(getenv("ABIN_QUANTILE_SINGLE"));
+                    !env_flag("ABIN_QUANTILE_SINGLE");
   p.n_strips = (int32_t)(pair ? (W + 2 * NT2 - 1) / (2 * NT2) : (W + NT - 1) / NT);
   const int64_t cols = (int64_t)p.n_strips * n_pages;
   // low quantiles of document pages sit where the strokes' grey levels end:
@@ -1242,8 +1257,7 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
   const int64_t slots = num_sms() * (int64_t)std::max(1, per_sm);
   int64_t B = H_out;
   double best = 1e300;
-  static const char* qwu_env = getenv("ABIN_Q_WU");  // experiments: warm-up row weight
-  const double qwu = qwu_env ? atof(qwu_env) : 0.5;
+  const double qwu = env_real("ABIN_Q_WU", 0.5, 0.0, 8.0);  // experiments: warm-up row weight
   for (int64_t nb = 1; nb <= std::max<int64_t>(1, H_out / 16); ++nb) {
     const int64_t Bc = (H_out + nb - 1) / nb;
     const int64_t waves = (cols * ((H_out + Bc - 1) / Bc) + slots - 1) / slots;
@@ -1343,10 +1357,9 @@ int run_host_io(int32_t method, const uint8_t* in, int64_t in_page_stride, uint8
   const int64_t dpage = dpitch * H, dopage = dopitch * H;
   // chunk of pages per stream and the number of streams in flight (tunable
   // for experiments through ABIN_HOSTIO_CHUNK_MB / ABIN_HOSTIO_STREAMS)
-  const int64_t chunk_mb = getenv("ABIN_HOSTIO_CHUNK_MB") ? atoll(getenv("ABIN_HOSTIO_CHUNK_MB")) : 64;
-  const int streams = getenv("ABIN_HOSTIO_STREAMS") ? atoi(getenv("ABIN_HOSTIO_STREAMS")) : 4;
-  const char* cb_env = getenv("ABIN_HOSTIO_CHUNK_BYTES");  // tests: tiny chunks force row bands
-  const int64_t target = cb_env ? std::max<long long>(1, atoll(cb_env)) : (std::max<int64_t>(1, chunk_mb) << 20);
+  const int64_t chunk_mb = env_int("ABIN_HOSTIO_CHUNK_MB", 64, 1, 1 << 16);
+  const int streams = (int)env_int("ABIN_HOSTIO_STREAMS", 4, 1, HostIoStreams::kMax);
+  const int64_t target = env_int("ABIN_HOSTIO_CHUNK_BYTES", chunk_mb << 20, 1, 1ll << 40);  // tests: tiny chunks
   // row bands for the methods whose band path needs nothing page-global
   // (Wolf / Feng only with a given L; the rules' global sums and Otsu never)
   const bool band_ok = method == ABIN_SAUVOLA || method == ABIN_NIBLACK || method == ABIN_QUANTILE ||
