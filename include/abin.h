@@ -191,12 +191,13 @@ int abin_bernsen(const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint
  *   ABIN_PHANSALKAR  {k, R, p, q}: t = m (1 + p e^(-q m) + k (s/R - 1))
  * The mask is the IEEE-double decision of every pixel (left-to-right
  * evaluation; pow/exp are the device's double routines, <= 2 ulp).  Within
- * h <= 129, w <= 127, Khurshid, Phansalkar with q >= 0 and Rais take the v5
- * kernel's exact integer window sums and certified fp32 filter (a bound on
- * the fp32 residual derived per parameter set -- for Rais per page, from
- * its M S -- DESIGN.md section 5) and decide in double only the pixels
- * inside the bound: the same mask.  Feng, Phansalkar with q < 0 and larger
- * windows run the v3 kernel (double for every pixel).  ABIN_EINVAL
+ * h <= 129, w <= 127, Khurshid, Phansalkar with q >= 0, Rais and Feng with
+ * gamma >= 1 take the v5 kernel's exact integer window sums and certified
+ * fp32 filter (a bound on the fp32 residual derived per parameter set -- for
+ * Rais per page, from its M S -- DESIGN.md section 5) and decide in double
+ * only the pixels inside the bound: the same mask.  Feng with gamma < 1,
+ * Phansalkar with q < 0 and larger windows run the v3 kernel (double for
+ * every pixel).  ABIN_EINVAL
  * for an unknown rule, missing or non-finite params, R <= 0. */
 int abin_binarize_rule(int32_t rule, const uint8_t* in, int64_t H, int64_t W, int64_t in_pitch, uint8_t* out,
                        int64_t out_pitch, int32_t mask_format, int32_t h, int32_t w, const double* params,

@@ -320,6 +320,48 @@ FilterConsts filter_consts_v5(int method, double k, double R, const double* rprm
   else if (method == M_NIBLACK || method == M_KHURSHID) { f.fa = 0.0f; f.fb = (float)k; }
   else { f.fa = (float)k; f.fb = (float)(1.0 / R); }
   f.delta1 = (float)(1.25 * (bound(ds) + eps64) + 1e-6);
+  if (method == M_FENG) {
+    // t = a1 m + k1 x^(1+g) (m - L) + k2 x^g L, x = s / R, g >= 1 (x^g Lipschitz on [0, X]); L <= 255.
+    // x~ = fl(s~ fl32(1/R)); x^g = ex2.approx(fl(g lg2.approx x~)): lg2.approx absolute error and
+    // ex2.approx relative error each taken as 2^-21, the product's rounding u g |lg2 x| (x^g |lg2 x|
+    // <= Z on [0, X]); x^(1+g) = fl(x^g x~); then the three terms and their sums, each rounded.
+    const double a1 = rprm[0], k1 = rprm[1], k2 = rprm[2], g = rprm[3], Rr = rprm[4];
+    const double iRf = (double)(float)(1.0 / Rr);
+    const double e_lg = std::ldexp(1.0, -21), e_ex = std::ldexp(1.0, -21), ln2 = 0.6931471805599453;
+    // the range of x~ and x (with the coarse |s~ - s| <= ds), and Z >= x^g |log2 x| on it
+    const double dxc = ds * iRf + 127.5 * 1.01 * u / Rr + u * (127.5 + ds) * iRf;
+    const double Xm = (127.5 + ds) * iRf * (1 + u) + dxc;
+    const double xs = std::exp(-1.0 / g);  // the maximiser of x^g |ln x| on (0, 1]
+    double Z = (xs <= Xm ? std::pow(xs, g) * (1.0 / g) / ln2 : std::pow(Xm, g) * std::fabs(std::log2(Xm)));
+    if (Xm > 1.0) Z = std::max(Z, std::pow(Xm, g) * std::log2(Xm));
+    const double Pg = std::pow(Xm, g);
+    // the bound as a function of the bound xs_ on |s~ - s| (affine in it: Xm, P0m, P1m use the coarse ds)
+    auto fb = [&](double xs_) {
+      const double dx = xs_ * iRf + 127.5 * 1.01 * u / Rr + u * (127.5 + ds) * iRf;
+      const double dP0 = g * std::pow(Xm, g - 1.0) * dx + 1.01 * ln2 * (Pg * g * e_lg + u * g * Z) * 1.01 +
+                         Pg * e_ex * 1.01 + std::ldexp(1.0, -126);
+      const double dP0c = g * std::pow(Xm, g - 1.0) * dxc + 1.01 * ln2 * (Pg * g * e_lg + u * g * Z) * 1.01 +
+                          Pg * e_ex * 1.01 + std::ldexp(1.0, -126);
+      const double P0m = Pg * (1 + 1e-5) + dP0c, P1m = P0m * Xm;
+      const double dP1 = dP0 * Xm + P0m * dx + 1.01 * u * P1m;
+      const double dT1 = std::fabs(a1) * dm + 2.02 * u * std::fabs(a1) * (255.0 + dm);
+      const double dT2 = std::fabs(k1) * (dP1 * 255.0 + P1m * (dm + 1.01 * u * 255.0)) +
+                         3.03 * u * std::fabs(k1) * P1m * (255.0 + dm);
+      const double dT3 = std::fabs(k2) * dP0 * 255.0 + 2.02 * u * std::fabs(k2) * P0m * 255.0;
+      const double tmax = (std::fabs(a1) + std::fabs(k1) * P1m + std::fabs(k2) * P0m) * (255.0 + dm);
+      return dT1 + dT2 + dT3 + 2.02 * u * tmax + 1.01 * u * (255.0 + tmax);
+    };
+    f.fa = (float)a1;
+    f.fb = (float)iRf;
+    f.delta1 = (float)(1.25 * (fb(ds) + eps64) + 1e-6);
+    // data-dependent form (as Niblack's): |s~ - s| <= min(sqrt dv, dv (1 + eps) / s~) + eps (smax + sqrt dv)
+    const double f0 = fb(0.0), f1 = fb(1.0) - f0, xe = eps_sqrt * (smax + rv);
+    f.rb0 = (float)((1.25 * (f0 + f1 * xe + eps64) + 1e-6) * (1 + 1e-6));
+    f.rb1 = (float)(1.25 * f1 * (1 + 1e-6));
+    f.rdv = (float)(dv * (1 + eps_sqrt) * (1 + 1e-6));
+    f.rsdv = (float)(rv * (1 + 1e-6));
+    return f;
+  }
   if (method == M_RAIS) {
     // t = m + 0.3 f s, f = (a - b) / max(a, b), a = m s, b = M S (the page's).  |df/da|, |df/db| <= 1/b
     // on both sides of a = b, so |f(a~, b~) - f| <= (|a~ - a| + |b~ - b|) / (b (1 - 2u)); f~'s own
@@ -363,17 +405,24 @@ FilterConsts filter_consts_v5(int method, double k, double R, const double* rprm
 // Khurshid 1/(h w) (N_mode 0); Phansalkar p and q log2(e)
 void rule_aux_v5(int method, const double* rprm, double hw, float* aux0, float* aux1) {
   *aux0 = *aux1 = 0.0f;
+  if (method == M_FENG) { *aux0 = (float)rprm[1]; *aux1 = (float)rprm[2]; }  // k1, k2 (gamma: aux2)
   if (method == M_KHURSHID) *aux0 = (float)(1.0 / hw);
   if (method == M_PHANSALKAR) { *aux0 = (float)rprm[2]; *aux1 = (float)(rprm[3] * 1.4426950408889634); }
 }
 
-// Khurshid, Phansalkar (q >= 0) and Rais run on v5 behind the certified
-// filter when its bound is usable (small against the 0.5 spacing of the
-// integer pixels; Rais's is formed per page from M S); Feng and other
-// parameters stay on the exact v3 path (Feng on v5's sums with its double
-// pow for every pixel measured slower than v3: 1.75 vs 1.51 ms per A4 page)
+// Khurshid, Phansalkar (q >= 0), Rais and Feng (gamma >= 1) run on v5 behind
+// the certified filter when its bound is usable (small against the 0.5
+// spacing of the integer pixels; Rais's is formed per page from M S); other
+// parameters stay on the exact v3 path
 bool rule_on_v5(int method, const double* rprm, double hw) {
   if (method == M_RAIS) return true;  // the bound is formed per page from M S (filter_consts_v5)
+  if (method == M_FENG) {  // gamma >= 1: x^gamma Lipschitz at 0; a bound small against the pixel spacing
+    for (int z = 0; z < 5; ++z)
+      if (!std::isfinite(rprm[z])) return false;
+    if (!(rprm[3] >= 1.0) || !(rprm[4] > 0.0)) return false;
+    const FilterConsts f = filter_consts_v5(method, 0.0, 1.0, rprm);
+    return std::isfinite(f.delta1) && f.delta1 < 8.0f;
+  }
   if (method != M_KHURSHID && method != M_PHANSALKAR) return false;
   for (int z = 0; z < 4; ++z)
     if (!std::isfinite(rprm[z])) return false;
@@ -782,6 +831,7 @@ int run_moments(const MomCall& c) {
         const FilterConsts f5 = filter_consts_v5(c.method, c.k, c.R, c.rprm);
         q.fa = f5.fa; q.fb = f5.fb; q.delta1 = f5.delta1;
         rule_aux_v5(c.method, c.rprm, (double)win.h * (double)win.w, &q.aux0, &q.aux1);
+        if (c.method == M_FENG) q.aux2 = (float)c.rprm[3];  // gamma
         if (c.method == M_RAIS) {  // the bounds' 1 / (M S) coefficients
           q.aux1 = f5.rais_c;
           q.aux0 = f5.rais_r0;
@@ -1771,9 +1821,10 @@ int abin_probe_filter(int32_t method, double k, double R, double L, const double
                       const uint32_t* d, const uint32_t* ncol, const uint32_t* nrow, const uint8_t* I, int64_t count,
                       float* e_out, float* s_out, double* bounds, void* stream) {
   if (count < 0) return ABIN_EINVAL;
-  const bool rule = method == ABIN_KHURSHID || method == ABIN_PHANSALKAR;
+  const bool rule = method == ABIN_KHURSHID || method == ABIN_PHANSALKAR || method == ABIN_FENG;
   if (!rule && method != ABIN_RAIS && (method < ABIN_SAUVOLA || method > ABIN_WOLF)) return ABIN_EINVAL;
   float aux0 = 0.0f, aux1 = 0.0f;
+  const float aux2 = method == ABIN_FENG && rule_params ? (float)rule_params[3] : 0.0f;
   int nmode = 0;
   float Lprobe = (float)L;
   if (method == ABIN_RAIS) {
@@ -1783,6 +1834,7 @@ int abin_probe_filter(int32_t method, double k, double R, double L, const double
   } else if (rule) {
     if (!rule_params) return ABIN_EINVAL;
     nmode = method == ABIN_KHURSHID && rule_params[1] != 0.0;
+    if (method == ABIN_FENG && !(std::isfinite(L) && L >= 0.0 && L <= 255.0)) return ABIN_EINVAL;
     const double hw = method == ABIN_KHURSHID && !nmode ? rule_params[2] : 1.0;  // Khurshid's N = h w
     if (!(hw >= 1.0)) return ABIN_EINVAL;
     if (!rule_on_v5(method, rule_params, hw)) return ABIN_ERANGE;  // not a parameter set v5 takes
@@ -1806,9 +1858,10 @@ int abin_probe_filter(int32_t method, double k, double R, double L, const double
   const unsigned nb = (unsigned)((count + 255) / 256);
   const float Lf = Lprobe;
 #define ABIN_PROBE(M) \
-  v5::k_probe<M><<<nb, 256, 0, st>>>(c, d, ncol, nrow, I, count, f.fa, f.fb, Lf, aux0, aux1, nmode, e_out, s_out)
+  v5::k_probe<M><<<nb, 256, 0, st>>>(c, d, ncol, nrow, I, count, f.fa, f.fb, Lf, aux0, aux1, aux2, nmode, e_out, s_out)
   if (method == M_SAUVOLA) ABIN_PROBE(M_SAUVOLA);
   else if (method == M_RAIS) ABIN_PROBE(M_RAIS);
+  else if (method == M_FENG) ABIN_PROBE(M_FENG);
   else if (method == M_NIBLACK) ABIN_PROBE(M_NIBLACK);
   else if (method == M_WOLF) ABIN_PROBE(M_WOLF);
   else if (method == M_KHURSHID) ABIN_PROBE(M_KHURSHID);

@@ -178,7 +178,8 @@ static __global__ void __launch_bounds__(kFixNT, 4) k_fixup(const MomParams p) {
       }
       if (is_rule(p.method)) {
         // v5 rules (Khurshid, Phansalkar): straight to the Table-1 row in IEEE double
-        const double tt = threshold_rule_fp64(p.method, c, d, n, p.rp, 0.0, page);
+        const double Lr = p.method == M_FENG ? (double)(p.L_fixed >= 0 ? p.L_fixed : (int)p.L_page[page]) : 0.0;
+        const double tt = threshold_rule_fp64(p.method, c, d, n, p.rp, Lr, page);
         const uint32_t mk = ((double)I <= tt) ? 0u : 1u;
         ++fb64;
         if (fabs((double)I - tt) < 1e-9) ++near;

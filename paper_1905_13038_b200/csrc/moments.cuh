@@ -89,6 +89,7 @@ struct MomParams {
   float maxs_margin;
   float aux0, aux1;          // v5 rules: Khurshid 1/(h w); Phansalkar p, q log2(e); Rais the bounds' 1/(M S) parts
   float rais_r1;             // Rais: the data-dependent bound's 1/(M S) slope part
+  float aux2;                // Feng: gamma (fa = a1, fb = 1/R, aux0 = k1, aux1 = k2)
   // statistics mode (page 0 only)
   uint64_t* c_out;
   uint64_t* d_out;

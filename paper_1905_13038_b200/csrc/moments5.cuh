@@ -153,6 +153,31 @@ __device__ __forceinline__ f2 residual2(f2 mn, f2 qn, f2 I, f2 fa2, f2 fb2, f2 L
   }
   const f2 wv = fma2(mn, mn, qn);  // m^2 - q = -v~
   s = pk(sqrt_approx(fabsf(lo(wv))), sqrt_approx(fabsf(hi(wv))));
+  if (METHOD == M_FENG) {
+    // t = a1 m + k1 x^(1+g) (m - L) + k2 x^g L, x = s/R (g >= 1): fa2 = a1, fb2 = (1/R, g),
+    // y2 = (k1, k2), Lf2 = L; x^g = ex2(g lg2 x) (0 at x = 0), x^(1+g) = x^g x; each operation
+    // rounded separately, as filter_consts_v5 bounds them
+    const float a1 = lo(fa2), iR = lo(fb2), g = hi(fb2), k1 = lo(y2), k2 = hi(y2), L = lo(Lf2);
+    float e[2];
+#pragma unroll
+    for (int z = 0; z < 2; ++z) {
+      const float m = -(z ? hi(mn) : lo(mn));
+      const float x = __fmul_rn(z ? hi(s) : lo(s), iR);
+      float P0 = 0.0f;
+      if (x > 0.0f) {
+        float lg, ex;
+        asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(x));
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex) : "f"(__fmul_rn(g, lg)));
+        P0 = ex;
+      }
+      const float P1 = __fmul_rn(P0, x);
+      const float T1 = __fmul_rn(a1, m);
+      const float T2 = __fmul_rn(__fmul_rn(k1, P1), __fsub_rn(m, L));
+      const float T3 = __fmul_rn(__fmul_rn(k2, P0), L);
+      e[z] = __fsub_rn(z ? hi(I) : lo(I), __fadd_rn(__fadd_rn(T1, T2), T3));
+    }
+    return pk(e[0], e[1]);
+  }
   if (METHOD == M_RAIS) {
     // t = m + 0.3 f s, f = (m s - M S) / max{m s, M S}  (Lf2 = fl32(M S), the page's; 0/0 -> 0, R16);
     // each operation rounded separately, as filter_consts_v5 bounds them
@@ -232,7 +257,7 @@ __device__ __forceinline__ f2 aux_operand(const MomParams& p, f2 Lf2, f2 nu) {
 template <int METHOD>
 __global__ void k_probe(const uint32_t* c, const uint32_t* d, const uint32_t* ncol, const uint32_t* nrow,
                         const uint8_t* I, int64_t count, float fa, float fb, float Lf, float aux0, float aux1,
-                        int nmode, float* e_out, float* s_out) {
+                        float aux2, int nmode, float* e_out, float* s_out) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= count) return;
   const float nu1 = -(__frcp_rn((float)ncol[q]) * __frcp_rn((float)nrow[q]));
@@ -242,10 +267,16 @@ __global__ void k_probe(const uint32_t* c, const uint32_t* d, const uint32_t* nc
   f2 x2 = splat(Lf);
   if (METHOD == M_KHURSHID) x2 = nmode ? mul2(nu, splat(-1.0f)) : splat(aux0);
   if (METHOD == M_PHANSALKAR) x2 = splat(aux0);
+  f2 y2 = splat(aux1);
+  if (METHOD == M_FENG) {
+    fa2 = splat(fa);
+    fb2 = pk(fb, aux2);
+    y2 = pk(aux0, aux1);
+  }
   const float If = (float)I[q];
   f2 sv;
   const f2 e = residual_pair<METHOD>(kBias + c[q], kBias + c[q], d[q], d[q], nu, nb, pk(If, If), fa2, fb2, x2, sv,
-                                     splat(aux1));
+                                     y2);
   e_out[q] = lo(e);
   if (s_out) s_out[q] = lo(sv);
 }
@@ -315,7 +346,8 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
   const int64_t Jend = min(J0 + (PACK ? (int64_t)kG * (G - KH) : (int64_t)p.Tw), p.W);
   const bool valid_lane = lane_ok && kl >= KH && j0 < Jend;
   const uint32_t vmask = valid_lane ? (Jend - j0 >= kG ? 0xFFFFu : ((1u << (uint32_t)(Jend - j0)) - 1u)) : 0u;
-  const float Lf = (METHOD == M_WOLF) ? (float)(p.L_fixed >= 0 ? p.L_fixed : (lane_ok ? (int)p.L_page[page] : 0)) : 0.0f;
+  const float Lf = (METHOD == M_WOLF || METHOD == M_FENG)
+                       ? (float)(p.L_fixed >= 0 ? p.L_fixed : (lane_ok ? (int)p.L_page[page] : 0)) : 0.0f;
   // Edge strips.  (1) -1/ncol per output column: ncol = w
   // except within (w+1)/2 columns of a border, so at most 10 lanes of a strip
   // see other counts; they get their own 16-entry slot of the table, every
@@ -443,12 +475,16 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
 
   f2 fa2, fb2;
   method_consts<METHOD>(p.fa, p.fb, fa2, fb2);
+  if (METHOD == M_FENG) {
+    fa2 = splat(p.fa);
+    fb2 = pk(p.fb, p.aux2);
+  }
   // Rais: the page's M S (fl32 of the double product) in the L slot, and the
   // certified bound delta1 + aux1 / (M S) (the fraction's derivative is <= 1 / (M S))
   const float MSf = METHOD == M_RAIS && lane_ok ? (float)(p.rp.MS[2 * page] * p.rp.MS[2 * page + 1]) : 0.0f;
   const f2 Lf2 = splat(METHOD == M_RAIS ? MSf : Lf);
   const float delta1 = METHOD == M_RAIS ? p.delta1 + p.aux1 / fmaxf(MSf, 1e-30f) : p.delta1;
-  const f2 y2 = splat(p.aux1);  // Phansalkar: q log2(e)
+  const f2 y2 = METHOD == M_FENG ? pk(p.aux0, p.aux1) : splat(p.aux1);  // Phansalkar: q log2(e); Feng: (k1, k2)
   // interior columns: ncol = w; per-row -1/n = -(1/w)(1/nrow) computed once per row
   const float inv_w = __frcp_rn((float)p.w);
   const int64_t in_pitch = p.in_pitch, out_pitch = p.out_pitch;
@@ -600,7 +636,8 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
           const f2 e = residual_pair<METHOD>(cq[0], cq[1], dq[0], dq[1], nu, nb, I, fa2, fb2,
                                              aux_operand<METHOD>(p, Lf2, nu), sv, y2);
           emin = fmin3(emin, fabsf(lo(e)), fabsf(hi(e)));
-          if (METHOD == M_NIBLACK || METHOD == M_KHURSHID || METHOD == M_RAIS) smin = fmin3(smin, lo(sv), hi(sv));
+          if (METHOD == M_NIBLACK || METHOD == M_KHURSHID || METHOD == M_RAIS || METHOD == M_FENG)
+            smin = fmin3(smin, lo(sv), hi(sv));
           e4[h2] = lo(e);
           e4[h2 + 1] = hi(e);
         }
@@ -627,7 +664,8 @@ __device__ __forceinline__ void mom5_body(const CUtensorMap& tin, const MomParam
           const float iMS = 1.0f / fmaxf(MSf, 1e-30f);
           const float rb0 = p.rb0 + p.aux0 * iMS, rb1 = p.rb1 + p.rais_r1 * iMS;
           if (emin * 0.999999f < (rb0 + rb1 * fminf(p.rsdv, p.rdv / smin)) * 1.000001f) amb = vmask;
-        } else if ((METHOD != M_NIBLACK && METHOD != M_KHURSHID) || emin * 0.999999f < v4::refined_bound(p, smin)) {
+        } else if ((METHOD != M_NIBLACK && METHOD != M_KHURSHID && METHOD != M_FENG) ||
+                   emin * 0.999999f < v4::refined_bound(p, smin)) {
           amb = vmask;
         }
       }

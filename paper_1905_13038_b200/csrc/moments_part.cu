@@ -78,6 +78,7 @@ cudaError_t launch_v5(const CUtensorMap& map, const CUtensorMap& mpk, const MomP
   if (p.method == M_KHURSHID) return launch_v5_m<W32, M_KHURSHID>(map, mpk, p, n_tiles, st);
   if (p.method == M_PHANSALKAR) return launch_v5_m<W32, M_PHANSALKAR>(map, mpk, p, n_tiles, st);
   if (p.method == M_RAIS) return launch_v5_m<W32, M_RAIS>(map, mpk, p, n_tiles, st);
+  if (p.method == M_FENG) return launch_v5_m<W32, M_FENG>(map, mpk, p, n_tiles, st);
   return launch_v5_m<W32, M_WOLF>(map, mpk, p, n_tiles, st);
 }
 

@@ -38,7 +38,11 @@ RULES = {"khurshid0": ("khurshid", (-0.1, 0, 16383.0)), "khurshid0s": ("khurshid
          # Rais {M S}: the page's product (the bound grows as 1 / (M S)): document pages (M S ~ 7e3),
          # dark / low-contrast pages, and a near-blank one
          "rais_ms7200": ("rais", (7200.0,)), "rais_ms900": ("rais", (900.0,)), "rais_ms40": ("rais", (40.0,)),
-         "rais_ms3": ("rais", (3.0,))}
+         "rais_ms3": ("rais", (3.0,)),
+         # Feng {a1, k1, k2, gamma, R} (gamma >= 1), page minimum FENG_L
+         "feng_g2": ("feng", (0.12, 0.015, 0.01, 2.0, 128.0)), "feng_g1": ("feng", (0.2, 0.05, 0.02, 1.0, 64.0)),
+         "feng_g3": ("feng", (0.1, 0.3, 0.1, 3.0, 100.0))}
+FENG_L = 37.0
 
 
 def t_exact(method, c, d, n, k, R, L):
@@ -49,6 +53,10 @@ def t_exact(method, c, d, n, k, R, L):
     s = np.sqrt(V.astype(LD) / (nl * nl))
     if method in RULES:
         rule, prm = RULES[method]
+        if rule == "feng":
+            a1, k1, k2, g, Rf = (LD(v) for v in prm)
+            x = s / Rf
+            return a1 * m + k1 * x ** (1 + g) * (m - LD(FENG_L)) + k2 * x ** g * LD(FENG_L)
         if rule == "rais":
             # t = m + 0.3 (m s - M S) / max{m s, M S} s  (0/0 -> 0, R16)
             a, b = m * s, LD(prm[0])
@@ -119,7 +127,7 @@ def run_probe(method, c, d, ncol, nrow, I):
     args = (dev(c, np.uint32), dev(d, np.uint32), dev(ncol, np.uint32), dev(nrow, np.uint32), dev(I, np.uint8))
     if method in RULES:
         rule, prm = RULES[method]
-        e, sv, b = abin.probe_filter(rule, *args, rule_params=prm)
+        e, sv, b = abin.probe_filter(rule, *args, L=FENG_L if rule == "feng" else 0.0, rule_params=prm)
     else:
         k, R, L = PARAMS[method]
         e, sv, b = abin.probe_filter(method, *args, k, R, L)
@@ -136,8 +144,8 @@ def check(method, c, d, ncol, nrow, I):
         coarse = b[0] + b[2] / RULES[method][1][0]   # the kernel's delta1 + aux1 / (M S)
     assert err.max() <= coarse, (method, err.max(), coarse)
     ratio = err.max() / coarse
-    if method == "niblack" or method.startswith("khurshid") or method.startswith("rais"):
-        # the data-dependent bound the kernel applies to Niblack / Khurshid / Rais lanes
+    if method == "niblack" or method.startswith(("khurshid", "rais", "feng")):
+        # the data-dependent bound the kernel applies to Niblack / Khurshid / Rais / Feng lanes
         with np.errstate(divide="ignore"):
             refined = b[1] + b[2] * np.minimum(b[4], b[3] / sv)
         assert (err <= refined).all(), (method, (err - refined).max())

@@ -104,9 +104,10 @@ def test_rules_outside_v5_stay_exact():
     check("khurshid", (-0.1, 0), I, 9, 201)
 
 
-# ---- Rais on v5 behind its certified filter (the bound formed per page from M S), and Feng
-# (the v3 kernel: the same masks either way)
-EXACT_SETS = {"feng": [(0.12, 0.015, 0.01, 2.0, 128.0), (0.2, 0.05, 0.02, 1.5, 64.0)], "rais": [()]}
+# ---- Rais (the bound formed per page from M S) and Feng (gamma >= 1) on v5 behind their
+# certified filters: the same masks as the v3 kernel's per-pixel double
+EXACT_SETS = {"feng": [(0.12, 0.015, 0.01, 2.0, 128.0), (0.2, 0.05, 0.02, 1.5, 64.0), (0.12, 0.015, 0.01, 0.5, 128.0)],
+              "rais": [()]}
 
 
 @pytest.mark.parametrize("rule", sorted(EXACT_SETS))
