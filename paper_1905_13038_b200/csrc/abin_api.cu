@@ -323,11 +323,12 @@ FilterConsts filter_consts_v5(int method, double k, double R, const double* rprm
   if (method == M_FENG) {
     // t = a1 m + k1 x^(1+g) (m - L) + k2 x^g L, x = s / R, g >= 1 (x^g Lipschitz on [0, X]); L <= 255.
     // x~ = fl(s~ fl32(1/R)); x^g = ex2.approx(fl(g lg2.approx x~)): lg2.approx absolute error and
-    // ex2.approx relative error each taken as 2^-21, the product's rounding u g |lg2 x| (x^g |lg2 x|
+    // ex2.approx relative error each taken as 2^-19, the product's rounding u g |lg2 x| (x^g |lg2 x|
     // <= Z on [0, X]); x^(1+g) = fl(x^g x~); then the three terms and their sums, each rounded.
     const double a1 = rprm[0], k1 = rprm[1], k2 = rprm[2], g = rprm[3], Rr = rprm[4];
     const double iRf = (double)(float)(1.0 / Rr);
-    const double e_lg = std::ldexp(1.0, -21), e_ex = std::ldexp(1.0, -21), ln2 = 0.6931471805599453;
+    // lg2.approx absolute and ex2.approx relative errors, taken as 2^-19 (as Phansalkar's ex2)
+    const double e_lg = std::ldexp(1.0, -19), e_ex = std::ldexp(1.0, -19), ln2 = 0.6931471805599453;
     // the range of x~ and x (with the coarse |s~ - s| <= ds), and Z >= x^g |log2 x| on it
     const double dxc = ds * iRf + 127.5 * 1.01 * u / Rr + u * (127.5 + ds) * iRf;
     const double Xm = (127.5 + ds) * iRf * (1 + u) + dxc;
