@@ -317,9 +317,12 @@ __device__ __forceinline__ void mom4_body(const CUtensorMap& tin, const MomParam
   auto load_centre = [&](const uint8_t* src, bool ok) -> uint4 {
     if (!ok || cmode == 0) return make_uint4(0, 0, 0, 0);
     if (!EDGE || cmode == 1) return __ldg(reinterpret_cast<const uint4*>(src));
-    uint32_t wd[4] = {0, 0, 0, 0};
+    // columns past W read as 255: their outputs are not stored, but a window
+    // wholly outside the image has c = 0 and t~ = 0, and I = 0 there would
+    // make the lane ambiguous (queued for the exact fixup) for nothing
+    uint32_t wd[4] = {~0u, ~0u, ~0u, ~0u};
     for (int t = 0; t < kG; ++t)
-      if (cx + t < p.W) wd[t >> 2] |= (uint32_t)__ldg(src + t) << (8 * (t & 3));
+      if (cx + t < p.W) wd[t >> 2] ^= (255u ^ (uint32_t)__ldg(src + t)) << (8 * (t & 3));
     return make_uint4(wd[0], wd[1], wd[2], wd[3]);
   };
   uint4 xc_next = load_centre(cptr, nrows > 0);

@@ -121,3 +121,23 @@ def test_batched_pages():
     out = ab.binarize_batched("sauvola", x, 61, 61, 0.5, 128.0)
     for p in range(P):
         assert np.array_equal(out[p].cpu().numpy(), oracle.binarize("sauvola", pages[p], 61, 61, 0.5, 128.0))
+
+
+
+@pytest.mark.parametrize("W", [2550, 2553, 1000])
+@pytest.mark.parametrize("hw", [9, 15])
+@pytest.mark.parametrize("v4", [False, True])
+def test_pad_columns_do_not_queue(W, hw, v4):
+    """Columns past W in the last lane of a row lie wholly outside the image
+    when w is small: their c = 0 gives t~ = 0 = I there.  They must not make
+    the lane ambiguous.  On a constant page Sauvola's t = m (1 - k) is far
+    from every pixel, so the exact fixup must see no pixel at all
+    (ABIN_COUNT_STAGES counts them; before the fix every row queued its last
+    lane), and the mask still equals the oracle's."""
+    I = np.full((128, W), 200, np.uint8)
+    x = to_dev(I)
+    cnt = torch.zeros(3, dtype=torch.int64, device=DEV)
+    flags = abin.COUNT_STAGES | (abin.V4_INTERNAL if v4 else 0)
+    got = run("sauvola", x, hw, hw, flags=flags, counters=cnt).cpu().numpy()
+    assert np.array_equal(got, oracle.binarize("sauvola", I, hw, hw, 0.5, 128.0))
+    assert cnt.tolist() == [0, 0, 0]
