@@ -395,12 +395,12 @@ def ours_main(args):
                     ab.sauvola(x0, h, w, k, R, packed=packed, out=o0, flags=flags, counters=counters)
             else:
                 ab.binarize_batched(method, x, h, w, k, R, packed=packed, out=o, flags=flags, counters=counters)
-        # quantile: the v5 kernel + its exact queue (q >= 0.2; the round-1
+        # quantile: the v5 kernel + its exact queue (q >= 0.25; the round-1
         # kernel alone below); moments: the v5 kernel + exact fixup (+ the v3
         # overflow follow-up when the queue could overflow: its CTAs exit at
         # once unless it did); Wolf adds the fill + global-minimum pre-pass
         if method == "quantile":
-            launches_per_step = 0 if P == 0 else (2 if k >= 0.2 else 1)
+            launches_per_step = 0 if P == 0 else (2 if k >= 0.25 else 1)
         else:
             launches_per_step = 0 if P == 0 else (5 if method == "wolf" else 3)
         if sweep:

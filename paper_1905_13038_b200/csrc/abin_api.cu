@@ -1231,13 +1231,15 @@ int run_quantile(int32_t method, const uint8_t* in, int64_t in_page_stride, int6
   if (method == ABIN_BERNSEN && !Q_out && !(flags & ABIN_Q2_INTERNAL))
     return run_bernsen(in, in_page_stride, n_pages, W, in_pitch, out, out_pitch, out_page_stride, fmt, win, q, row0,
                        H_out, H_global, buf_row0, st);
-  // v5 (quantile5.cuh) for masks at q >= 0.2; low quantiles of document
+  // v5 (quantile5.cuh) for masks at q >= 0.25; low quantiles of document
   // pages sit in either the strokes' or the background's levels, which a few
   // 16-level windows per tile do not cover (measured: 1-35 % of the pixels to
-  // the exact queue at q = 0.1), so they keep the round-1 kernels.
+  // the exact queue at q = 0.1), so they keep the round-1 kernels (config-5
+  // page, tools/dev/q5_low.py: at q = 0.2 round-1 1.16 ms, v5 1.23-1.46 ms;
+  // at q = 0.25 v5 0.70 ms, round-1 1.06 ms).
   // ABIN_Q5_ALWAYS (tests) takes v5 for every q.
   const bool q5_always = env_flag("ABIN_Q5_ALWAYS");
-  if (method == ABIN_QUANTILE && !Q_out && !(flags & ABIN_Q2_INTERNAL) && (q >= 0.2 || q5_always)) {
+  if (method == ABIN_QUANTILE && !Q_out && !(flags & ABIN_Q2_INTERNAL) && (q >= 0.25 || q5_always)) {
     const int rc = run_quant5(in, in_page_stride, n_pages, W, in_pitch, out, out_pitch, out_page_stride, fmt, win, q,
                               row0, H_out, H_global, buf_rows, buf_row0, st, counters);
     if (rc >= 0) return rc;

@@ -29,7 +29,7 @@ DEV = torch.device("cuda:0")
 
 @pytest.fixture(autouse=True)
 def _v5_for_every_q(monkeypatch):
-    # the library keeps q < 0.2 on the round-1 kernels; here v5 takes every q
+    # the library keeps q < 0.25 on the round-1 kernels; here v5 takes every q
     monkeypatch.setenv("ABIN_Q5_ALWAYS", "1")
 
 
