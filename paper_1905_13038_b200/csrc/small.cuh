@@ -4,14 +4,15 @@
 // built for throughput -- one warp walks a band of rows through a TMA ring
 // -- and on a single small page its time is the latency of a lone warp's
 // rows (config 1, 512^2: ~19 us for k_mom5 plus the exact-fixup launch).
-// Here a CTA of 128 threads takes a 16 x 128 output tile:
+// Here a CTA of 256 threads takes a 16 x 128 output tile:
 //   1. the tile's input region (16 + h - 1 rows x 128 + w - 1 columns; 0
 //      outside the image) is loaded into shared memory;
 //   2. vertical window sums C, D of every region column for the 16 output
 //      rows by the recursion of PAPER.md:107-110 (a thread per column, exact
 //      uint32: 255^2 h < 2^32);
-//   3. horizontal window sums c, d per output pixel by the row recursion of
-//      PAPER.md:119-120 (a thread per 16 outputs of a row, exact uint32), the
+//   3. horizontal window sums c, d per output pixel as
+//      differences of per-row prefix sums of C, D (exact uint32; a warp per
+//      two rows, a lane per column of each 32-column group), the
 //      count n of Alg. 1 l.118, and the decision: the certified fp32 residual
 //      of the v5 kernel (residual_pair, bound delta1 of filter_consts_v5) and,
 //      for a pixel inside the bound, the canonical IEEE-double threshold
@@ -26,7 +27,9 @@
 namespace abin {
 namespace sm {
 
-constexpr int kTH = 16, kTW = 128, kNT = 128;
+constexpr int kTH = 16, kTW = 128, kNT = 256;
+constexpr int kRPW = kTH / (kNT / 32);  // output rows per warp in steps 2b, 3
+static_assert(kRPW * (kNT / 32) == kTH && kTW % 64 == 0, "step 3: a warp takes kRPW rows, a lane pairs of 32-column groups");
 constexpr int kMaxWin = 64;  // h, w (effective) of the small path
 
 struct SmallParams {
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
     const int nch = (dx + RW + 15) >> 4;
     const bool vec = ((reinterpret_cast<uintptr_t>(p.in) | (uintptr_t)p.in_pitch | (uintptr_t)p.in_page_stride) &
                       15u) == 0;
-    for (int idx = tid; idx < RH * nch; idx += kNT) {
+    auto fetch = [&](int idx) {
       const int ry = idx / nch, ch = idx - ry * nch;
       const int64_t y = y0 + ry, x = xa + 16 * ch;
       uint4 v = make_uint4(0u, 0u, 0u, 0u);
@@ -95,7 +98,26 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
           v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
         }
       }
-      *reinterpret_cast<uint4*>(reg + ry * RWp + 16 * ch) = v;
+      return v;
+    };
+    // kLD chunks in flight per thread (a lone CTA per SM: the loads' latency is the cost)
+    constexpr int kLD = 4;
+    const int N = RH * nch;
+    for (int base = tid; base < N; base += kLD * kNT) {
+      uint4 v[kLD];
+#pragma unroll
+      for (int k = 0; k < kLD; ++k) {
+        const int idx = base + k * kNT;
+        v[k] = idx < N ? fetch(idx) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int k = 0; k < kLD; ++k) {
+        const int idx = base + k * kNT;
+        if (idx < N) {
+          const int ry = idx / nch, ch = idx - ry * nch;
+          *reinterpret_cast<uint4*>(reg + ry * RWp + 16 * ch) = v[k];
+        }
+      }
     }
   }
   __syncthreads();
@@ -120,74 +142,108 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
     }
   }
   __syncthreads();
-  // 3. a thread = 16 outputs of one row: horizontal sums, then the decision
-  const int t = tid >> 3, seg = tid & 7;
-  const int64_t i = i0 + t;
-  const int64_t jb = j0 + 16 * seg;
-  if (i >= p.row0 + p.H_out || jb >= p.W) return;
-  const uint32_t* Cr = Cs + t * CWp + 16 * seg;
-  const uint32_t* Dr = Ds + t * CWp + 16 * seg;
-  uint32_t c = 0, d = 0;
-#pragma unroll 4
-  for (int x = 0; x < p.w; ++x) {
-    c += Cr[x];
-    d += Dr[x];
+  // 2b. each warp turns its kRPW rows of C and D into exclusive prefix sums
+  // along the row (RW + 1 entries: P[x] = C[0] + .. + C[x-1], uint32 wraps
+  // cancel in differences), so that the window sums of PAPER.md:119-120 are
+  // c(j) = P[j + w] - P[j] for any thread-to-column mapping: step 3 reads
+  // consecutive words per warp (no bank conflicts) instead of running the
+  // row recursion over a thread's own 16-column segment.
+  const int wid = tid >> 5, lane = tid & 31;
+  {
+    const int NP = RW + 1;
+    const int chunk = (NP + 31) >> 5;  // <= 6 (RW <= 128 + 64 - 1)
+#pragma unroll 1
+    for (int q = 0; q < 2 * kRPW; ++q) {
+      uint32_t* A = ((q & 1) ? Ds : Cs) + (kRPW * wid + (q >> 1)) * CWp;
+      uint32_t v[6], sum = 0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const int idx = lane * chunk + k;
+        v[k] = (k < chunk && idx < RW) ? A[idx] : 0u;
+        sum += v[k];
+      }
+      uint32_t inc = sum;
+#pragma unroll
+      for (int dlt = 1; dlt < 32; dlt <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, dlt);
+        if (lane >= dlt) inc += y;
+      }
+      uint32_t run = inc - sum;
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const int idx = lane * chunk + k;
+        if (k < chunk && idx < NP) A[idx] = run;
+        run += v[k];
+      }
+    }
   }
-  const uint32_t nrow = (uint32_t)(min(i + p.u, p.H_global - 1) - max(i - p.o, (int64_t)-1));
-  const float inv_nrow = __frcp_rn((float)nrow);
+  __syncwarp();
+  // 3. a warp = its kRPW rows; a lane = the columns lane, lane + 32, lane + 64,
+  // lane + 96 of the tile: window sums from the prefix rows, then the decision
   const float Lf = METHOD == M_WOLF ? (float)(p.L_fixed >= 0 ? p.L_fixed : (int)p.L_page[page]) : 0.0f;
   v5::f2 fa2, fb2;
   v5::method_consts<METHOD>(p.fa, p.fb, fa2, fb2);
   const v5::f2 Lf2 = v5::splat(Lf);
-  const uint8_t* irow = pg + (i - p.buf_row0) * p.in_pitch;
   unsigned long long near = 0, fb64 = 0;
-  uint32_t bits = 0;
-  uint8_t* orow = p.out + (int64_t)page * p.out_page_stride + (i - p.row0) * p.out_pitch;
-  const int nval = (int)min((int64_t)16, p.W - jb);
 #pragma unroll 1
-  for (int s2 = 0; s2 < 16; s2 += 2) {
-    uint32_t cq[2], dq[2], nq[2];
-    float nuv[2];
+  for (int rr = 0; rr < kRPW; ++rr) {
+    const int t = kRPW * wid + rr;
+    const int64_t i = i0 + t;
+    if (i >= p.row0 + p.H_out) break;  // warp-uniform
+    const uint32_t* Pc = Cs + t * CWp;
+    const uint32_t* Pd = Ds + t * CWp;
+    const uint32_t nrow = (uint32_t)(min(i + p.u, p.H_global - 1) - max(i - p.o, (int64_t)-1));
+    const float inv_nrow = __frcp_rn((float)nrow);
+    // the centre pixels from the staged region (row t + o - 1, column l - 1 + tile column)
+    const uint8_t* irow = reg + (t + p.o - 1) * RWp + dx + (p.l - 1);
+    uint8_t* orow = p.out + (int64_t)page * p.out_page_stride + (i - p.row0) * p.out_pitch;
+#pragma unroll 1
+    for (int q2 = 0; q2 < kTW / 32; q2 += 2) {
+      uint32_t cq[2], dq[2], nq[2], Iz[2];
+      float nuv[2];
+      bool ok[2];
 #pragma unroll
-    for (int z = 0; z < 2; ++z) {
-      const int s = s2 + z;
-      const int64_t j = jb + s;
-      cq[z] = c;
-      dq[z] = d;
-      const uint32_t ncol = (uint32_t)(min(j + p.r, p.W - 1) - max(j - p.l, (int64_t)-1));
-      nq[z] = ncol * nrow;
-      nuv[z] = -(__frcp_rn((float)ncol) * inv_nrow);
-      // slide to output s + 1: c += C[s + w] - C[s] (region columns of this segment)
-      c += Cr[s + p.w] - Cr[s];
-      d += Dr[s + p.w] - Dr[s];
-    }
-    const v5::f2 nu = v5::pk(nuv[0], nuv[1]);
-    const v5::f2 nb = v5::mul2(nu, v5::splat(-8388608.0f));
-    const uint32_t Ia = s2 < nval ? irow[jb + s2] : 0u, Ib = s2 + 1 < nval ? irow[jb + s2 + 1] : 0u;
-    v5::f2 sv;
-    const v5::f2 e = v5::residual_pair<METHOD>(v5::kBias + cq[0], v5::kBias + cq[1], dq[0], dq[1], nu, nb,
-                                               v5::pk((float)Ia, (float)Ib), fa2, fb2, Lf2, sv);
-    const float ez[2] = {v5::lo(e), v5::hi(e)};
-    const uint32_t Iz[2] = {Ia, Ib};
-#pragma unroll
-    for (int z = 0; z < 2; ++z) {
-      if (s2 + z >= nval) continue;
-      uint32_t mk;
-      if (fabsf(ez[z]) >= p.delta1) {
-        mk = ez[z] < 0.0f ? 0u : 1u;  // e = I - t~ < 0: I < t, foreground (0)
-      } else {
-        const double tt = threshold_fp64(METHOD, cq[z], dq[z], nq[z], p.k, p.R, (double)Lf);
-        mk = ((double)Iz[z] <= tt) ? 0u : 1u;
-        ++fb64;
-        if (fabs((double)Iz[z] - tt) < 1e-9) ++near;
+      for (int z = 0; z < 2; ++z) {
+        const int jj = 32 * (q2 + z) + lane;
+        const int64_t j = j0 + jj;
+        ok[z] = j < p.W;
+        cq[z] = Pc[jj + p.w] - Pc[jj];
+        dq[z] = Pd[jj + p.w] - Pd[jj];
+        const uint32_t ncol = ok[z] ? (uint32_t)(min(j + p.r, p.W - 1) - max(j - p.l, (int64_t)-1)) : 1u;
+        nq[z] = ncol * nrow;
+        nuv[z] = -(__frcp_rn((float)ncol) * inv_nrow);
+        Iz[z] = ok[z] ? irow[jj] : 0u;
       }
-      if (p.fmt == 0) orow[jb + s2 + z] = (uint8_t)mk;
-      else bits |= mk << (15 - (s2 + z));
+      const v5::f2 nu = v5::pk(nuv[0], nuv[1]);
+      const v5::f2 nb = v5::mul2(nu, v5::splat(-8388608.0f));
+      v5::f2 sv;
+      const v5::f2 e = v5::residual_pair<METHOD>(v5::kBias + cq[0], v5::kBias + cq[1], dq[0], dq[1], nu, nb,
+                                                 v5::pk((float)Iz[0], (float)Iz[1]), fa2, fb2, Lf2, sv);
+      const float ez[2] = {v5::lo(e), v5::hi(e)};
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+        uint32_t mk = 0u;
+        if (ok[z]) {
+          if (fabsf(ez[z]) >= p.delta1) {
+            mk = ez[z] < 0.0f ? 0u : 1u;  // e = I - t~ < 0: I < t, foreground (0)
+          } else {
+            const double tt = threshold_fp64(METHOD, cq[z], dq[z], nq[z], p.k, p.R, (double)Lf);
+            mk = ((double)Iz[z] <= tt) ? 0u : 1u;
+            ++fb64;
+            if (fabs((double)Iz[z] - tt) < 1e-9) ++near;
+          }
+        }
+        const int64_t jq = j0 + 32 * (q2 + z);  // first column of this 32-column group
+        if (p.fmt == 0) {
+          if (ok[z]) orow[jq + lane] = (uint8_t)mk;
+        } else {
+          // bit mask, MSB first: lane L's bit is column jq + L, byte b holds columns 8 b .. 8 b + 7
+          const uint32_t word = __brev(__ballot_sync(0xffffffffu, mk != 0u));
+          if (lane < 4 && jq + 8 * lane < p.W) orow[(jq >> 3) + lane] = (uint8_t)(word >> (24 - 8 * lane));
+        }
+      }
     }
-  }
-  if (p.fmt != 0) {
-    orow[jb >> 3] = (uint8_t)(bits >> 8);
-    if (nval > 8) orow[(jb >> 3) + 1] = (uint8_t)(bits & 0xFFu);
   }
   if (p.counters) {
     if (near) atomicAdd(&p.counters[0], near);
