@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
   v5::method_consts<METHOD>(p.fa, p.fb, fa2, fb2);
   const v5::f2 Lf2 = v5::splat(Lf);
   unsigned long long near = 0, fb64 = 0;
+  const int Wi = (int)p.W, j0i = (int)j0;
 #pragma unroll 1
   for (int rr = 0; rr < kRPW; ++rr) {
     const int t = kRPW * wid + rr;
@@ -206,11 +207,11 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
 #pragma unroll
       for (int z = 0; z < 2; ++z) {
         const int jj = 32 * (q2 + z) + lane;
-        const int64_t j = j0 + jj;
-        ok[z] = j < p.W;
+        const int j = j0i + jj;  // the small path's pages have W < 2^30 (run_small)
+        ok[z] = j < Wi;
         cq[z] = Pc[jj + p.w] - Pc[jj];
         dq[z] = Pd[jj + p.w] - Pd[jj];
-        const uint32_t ncol = ok[z] ? (uint32_t)(min(j + p.r, p.W - 1) - max(j - p.l, (int64_t)-1)) : 1u;
+        const uint32_t ncol = ok[z] ? (uint32_t)(min(j + p.r, Wi - 1) - max(j - p.l, -1)) : 1u;
         nq[z] = ncol * nrow;
         nuv[z] = -(__frcp_rn((float)ncol) * inv_nrow);
         Iz[z] = ok[z] ? irow[jj] : 0u;
@@ -234,13 +235,13 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
             if (fabs((double)Iz[z] - tt) < 1e-9) ++near;
           }
         }
-        const int64_t jq = j0 + 32 * (q2 + z);  // first column of this 32-column group
+        const int jq = j0i + 32 * (q2 + z);  // first column of this 32-column group
         if (p.fmt == 0) {
           if (ok[z]) orow[jq + lane] = (uint8_t)mk;
         } else {
           // bit mask, MSB first: lane L's bit is column jq + L, byte b holds columns 8 b .. 8 b + 7
           const uint32_t word = __brev(__ballot_sync(0xffffffffu, mk != 0u));
-          if (lane < 4 && jq + 8 * lane < p.W) orow[(jq >> 3) + lane] = (uint8_t)(word >> (24 - 8 * lane));
+          if (lane < 4 && jq + 8 * lane < Wi) orow[(jq >> 3) + lane] = (uint8_t)(word >> (24 - 8 * lane));
         }
       }
     }

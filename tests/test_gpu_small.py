@@ -1,5 +1,5 @@
 """GPU parity (-m gpu) of the small-call kernel (csrc/small.cuh): single small
-pages (here up to 2^19 pixels, windows up to 64 x 64) go to one launch of a
+pages (here up to 2^21 pixels, windows up to 64 x 64) go to one launch of a
 shared-memory tile kernel -- exact integer window sums, the certified fp32
 residual and the canonical double threshold inline.  Masks and near-tie
 counts must equal the oracle's bit for bit: odd / even windows, windows
@@ -97,3 +97,25 @@ def test_small_kernel_bands_and_streaming_twin(monkeypatch):
     monkeypatch.setenv("ABIN_SMALL_PX", "0")
     b = ab.sauvola(x, 31, 25).cpu().numpy()
     assert np.array_equal(a, b) and np.array_equal(a, whole)
+
+
+def test_small_kernel_megapixel_page(monkeypatch):
+    # the size limit is 2^21 pixels for windows up to 32 x 32 (2^20 beyond): a
+    # ragged 1.43 Mpx page (9 x 69 tiles + partial tiles) against the oracle and
+    # the streaming kernels, byte and bit masks
+    J = synth.page(1100, 1301, synth.config_seed(2, 3))
+    x = to_dev(J)
+    for (h, w) in ((32, 32), (15, 17)):
+        ref = oracle.binarize("sauvola", J, h, w, 0.5, 128.0)
+        a = ab.sauvola(x, h, w).cpu().numpy()
+        ab_bits = ab.sauvola(x, h, w, packed=True).cpu().numpy()
+        monkeypatch.setenv("ABIN_SMALL_PX", "0")
+        b = ab.sauvola(x, h, w).cpu().numpy()
+        monkeypatch.delenv("ABIN_SMALL_PX")
+        assert np.array_equal(a, ref) and np.array_equal(b, ref), (h, w)
+        assert np.array_equal(ab_bits, oracle.pack_bits(ref)), (h, w)
+    # 61 x 61 on the same page is past the 2^20 limit of the wide windows: both routes agree
+    ref = oracle.binarize("wolf", J, 61, 61, 0.5, 128.0)
+    assert np.array_equal(ab.wolf(x, 61, 61, 0.5, 128.0).cpu().numpy(), ref)
+    K = np.ascontiguousarray(J[:800])   # 1.04 Mpx <= 2^20: the tile kernel at 61 x 61
+    assert np.array_equal(ab.wolf(to_dev(K), 61, 61, 0.5, 128.0).cpu().numpy(), oracle.binarize("wolf", K, 61, 61, 0.5, 128.0))
