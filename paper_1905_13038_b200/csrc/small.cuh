@@ -56,15 +56,18 @@ __host__ __device__ inline size_t smem_bytes(int RWp, int CWp, int h) {
   return region_bytes(RWp, h) + (size_t)2 * kTH * CWp * 4;
 }
 
+#ifndef ABIN_SMALL_MINB
+#define ABIN_SMALL_MINB 4  // resident CTAs per SM the register budget is set for (64 registers; 1: 80 registers, 1024^2 pages 15 % slower)
+#endif
 template <int METHOD>
-__global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
+__global__ void __launch_bounds__(kNT, ABIN_SMALL_MINB) k_small(const SmallParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int tid = threadIdx.x;
-  int64_t b = blockIdx.x;
-  const int ct = (int)(b % p.n_ct);
-  b /= p.n_ct;
-  const int rt = (int)(b % p.n_rt);
-  const int page = (int)(b / p.n_rt);
+  uint32_t b = blockIdx.x;  // < 2^31 tiles: 32-bit divisions
+  const int ct = (int)(b % (uint32_t)p.n_ct);
+  b /= (uint32_t)p.n_ct;
+  const int rt = (int)(b % (uint32_t)p.n_rt);
+  const int page = (int)(b / (uint32_t)p.n_rt);
   const int64_t i0 = p.row0 + (int64_t)rt * kTH, j0 = (int64_t)ct * kTW;
   const int RH = kTH + p.h - 1, RW = kTW + p.w - 1, RWp = p.RWp, CWp = p.CWp;
   uint8_t* reg = smem;                                                 // [RH][RWp]
@@ -82,13 +85,20 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
     const int nch = (dx + RW + 15) >> 4;
     const bool vec = ((reinterpret_cast<uintptr_t>(p.in) | (uintptr_t)p.in_pitch | (uintptr_t)p.in_page_stride) &
                       15u) == 0;
-    auto fetch = [&](int idx) {
-      const int ry = idx / nch, ch = idx - ry * nch;
-      const int64_t y = y0 + ry, x = xa + 16 * ch;
+    // a 16-lane group per region row, a lane per 16-byte chunk (nch <= 13), 16
+    // rows per pass: no index divisions.  x is a multiple of 16, so a chunk
+    // left of the image is wholly outside; chunk classes: 0 zeros, 1 one
+    // 16-byte load, 2 byte loads (the chunk holding column W, unaligned rows)
+    const int ch = tid & 15, rg = tid >> 4;
+    const int64_t x = xa + 16 * ch;
+    const bool ch_ok = ch < nch;
+    const int cls = (!ch_ok || x + 16 <= 0 || x >= p.W) ? 0 : ((vec && x + 16 <= p.W) ? 1 : 2);
+    auto fetch = [&](int ry) {
+      const int64_t y = y0 + ry;
       uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      if (y >= 0 && y < p.H_global) {
+      if (cls != 0 && y >= 0 && y < p.H_global) {
         const uint8_t* row = pg + (y - p.buf_row0) * p.in_pitch;
-        if (vec && x >= 0 && x + 16 <= p.W) {
+        if (cls == 1) {
           v = __ldg(reinterpret_cast<const uint4*>(row + x));
         } else {
           uint32_t wv[4] = {0u, 0u, 0u, 0u};
@@ -100,23 +110,19 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
       }
       return v;
     };
-    // kLD chunks in flight per thread (a lone CTA per SM: the loads' latency is the cost)
+    // kLD rows in flight per thread (a lone CTA per SM: the loads' latency is the cost)
     constexpr int kLD = 4;
-    const int N = RH * nch;
-    for (int base = tid; base < N; base += kLD * kNT) {
+    for (int r0 = rg; r0 < RH; r0 += kLD * (kNT / 16)) {
       uint4 v[kLD];
 #pragma unroll
       for (int k = 0; k < kLD; ++k) {
-        const int idx = base + k * kNT;
-        v[k] = idx < N ? fetch(idx) : make_uint4(0u, 0u, 0u, 0u);
+        const int ry = r0 + k * (kNT / 16);
+        v[k] = ry < RH ? fetch(ry) : make_uint4(0u, 0u, 0u, 0u);
       }
 #pragma unroll
       for (int k = 0; k < kLD; ++k) {
-        const int idx = base + k * kNT;
-        if (idx < N) {
-          const int ry = idx / nch, ch = idx - ry * nch;
-          *reinterpret_cast<uint4*>(reg + ry * RWp + 16 * ch) = v[k];
-        }
+        const int ry = r0 + k * (kNT / 16);
+        if (ry < RH && ch_ok) *reinterpret_cast<uint4*>(reg + ry * RWp + 16 * ch) = v[k];
       }
     }
   }
@@ -150,8 +156,8 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
   // row recursion over a thread's own 16-column segment.
   const int wid = tid >> 5, lane = tid & 31;
   {
-    const int NP = RW + 1;
-    const int chunk = (NP + 31) >> 5;  // <= 6 (RW <= 128 + 64 - 1)
+    const int NP = RW + 1;             // <= 192 = 32 lanes x 6 (RW <= 128 + 64 - 1)
+    constexpr int chunk = 6;
 #pragma unroll 1
     for (int q = 0; q < 2 * kRPW; ++q) {
       uint32_t* A = ((q & 1) ? Ds : Cs) + (kRPW * wid + (q >> 1)) * CWp;
@@ -159,7 +165,7 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
 #pragma unroll
       for (int k = 0; k < 6; ++k) {
         const int idx = lane * chunk + k;
-        v[k] = (k < chunk && idx < RW) ? A[idx] : 0u;
+        v[k] = idx < RW ? A[idx] : 0u;
         sum += v[k];
       }
       uint32_t inc = sum;
@@ -173,7 +179,7 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
 #pragma unroll
       for (int k = 0; k < 6; ++k) {
         const int idx = lane * chunk + k;
-        if (k < chunk && idx < NP) A[idx] = run;
+        if (idx < NP) A[idx] = run;
         run += v[k];
       }
     }
@@ -187,6 +193,16 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
   const v5::f2 Lf2 = v5::splat(Lf);
   unsigned long long near = 0, fb64 = 0;
   const int Wi = (int)p.W, j0i = (int)j0;
+  // the lane's columns are the same in every row: their counts (Alg. 1 l.118) and reciprocals once
+  uint32_t ncl[kTW / 32];
+  float rcol[kTW / 32];
+#pragma unroll
+  for (int q = 0; q < kTW / 32; ++q) {
+    const int j = j0i + 32 * q + lane;
+    ncl[q] = j < Wi ? (uint32_t)(min(j + p.r, Wi - 1) - max(j - p.l, -1)) : 1u;
+    rcol[q] = __frcp_rn((float)ncl[q]);
+  }
+  uint8_t* orow = p.out + (int64_t)page * p.out_page_stride + (i0 + kRPW * wid - p.row0) * p.out_pitch - p.out_pitch;
 #pragma unroll 1
   for (int rr = 0; rr < kRPW; ++rr) {
     const int t = kRPW * wid + rr;
@@ -198,8 +214,8 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
     const float inv_nrow = __frcp_rn((float)nrow);
     // the centre pixels from the staged region (row t + o - 1, column l - 1 + tile column)
     const uint8_t* irow = reg + (t + p.o - 1) * RWp + dx + (p.l - 1);
-    uint8_t* orow = p.out + (int64_t)page * p.out_page_stride + (i - p.row0) * p.out_pitch;
-#pragma unroll 1
+    orow += p.out_pitch;
+#pragma unroll
     for (int q2 = 0; q2 < kTW / 32; q2 += 2) {
       uint32_t cq[2], dq[2], nq[2], Iz[2];
       float nuv[2];
@@ -211,9 +227,8 @@ __global__ void __launch_bounds__(kNT) k_small(const SmallParams p) {
         ok[z] = j < Wi;
         cq[z] = Pc[jj + p.w] - Pc[jj];
         dq[z] = Pd[jj + p.w] - Pd[jj];
-        const uint32_t ncol = ok[z] ? (uint32_t)(min(j + p.r, Wi - 1) - max(j - p.l, -1)) : 1u;
-        nq[z] = ncol * nrow;
-        nuv[z] = -(__frcp_rn((float)ncol) * inv_nrow);
+        nq[z] = ncl[q2 + z] * nrow;
+        nuv[z] = -(rcol[q2 + z] * inv_nrow);
         Iz[z] = ok[z] ? irow[jj] : 0u;
       }
       const v5::f2 nu = v5::pk(nuv[0], nuv[1]);

@@ -1,13 +1,18 @@
 """Per-source-line instruction / stall summary of an ncu report (dev tool).
 The report's SASS page is mapped to source lines with a locally compiled
 cubin of the same kernel (nvdisasm -g):
-python tools/dev/ncu_lines.py report.ncu-rep kernel.cubin px [top]"""
+python tools/dev/ncu_lines.py report.ncu-rep kernel.cubin px [top [function-name substring]]"""
 import collections, csv, io, re, subprocess, sys
 rep, cubin, px = sys.argv[1], sys.argv[2], float(sys.argv[3])
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+func = sys.argv[5] if len(sys.argv) > 5 else None  # cubins with several kernels: the .text section to map
 sass = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
-line = None; fn = None; off2 = {}
+line = None; fn = None; off2 = {}; inside = func is None
 for l in sass.split("\n"):
+    if func is not None and l.lstrip().startswith(".section"):
+        inside = (".text." in l and func in l); line = None; continue
+    if not inside:
+        continue
     m = re.search(r'File "([^"]+)", line (\d+)', l)
     if m:
         fn, line = m.group(1).split("/")[-1], int(m.group(2)); continue
