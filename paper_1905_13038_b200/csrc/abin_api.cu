@@ -637,10 +637,11 @@ int run_small(const MomCall& c, const Window& win) {
   const uint32_t forced = ABIN_FORCE_FP64 | ABIN_FORCE_U64_SQ | ABIN_V3_INTERNAL | ABIN_V4_INTERNAL |
                           ABIN_NO_TMA_INTERNAL;
   // Size limit of the tile kernel, measured against the streaming kernels on one
-  // page (tools/dev/small_big.py: 1024^2 14.4 vs 27.9 us at 15 x 15, 19.1 vs
-  // 31.9 at 63 x 63; 2048^2 34.9 vs 31.8 and 46.1 vs 36.0): 2^21 pixels for
-  // windows up to 32 x 32, 2^20 beyond.  ABIN_SMALL_PX: tests / experiments (0: off).
-  const int64_t max_px = env_int("ABIN_SMALL_PX", (win.h <= 32 && win.w <= 32) ? 1ll << 21 : 1ll << 20, 0, 1ll << 30);
+  // page (tools/dev/small_big.py, us per call at 15 / 31 / 63 windows): 1024^2
+  // 10.3 / 10.3 / 12.4 vs 27.9 / 27.7 / 31.9; 2048^2 26.7 / 28.8 / 33.6 vs 31.9 /
+  // 31.7 / 35.9; 3300 x 2550 53 / 56 / 68 vs 45 / 44 / 51: 2^22 pixels.
+  // ABIN_SMALL_PX: tests / experiments (0: off).
+  const int64_t max_px = env_int("ABIN_SMALL_PX", 1ll << 22, 0, 1ll << 30);
   if (stats || (c.flags & forced) || win.h > kMaxWin || win.w > kMaxWin ||
       !(c.method == M_SAUVOLA || c.method == M_NIBLACK || c.method == M_WOLF) ||
       c.n_pages * c.H_out * c.W > max_px)

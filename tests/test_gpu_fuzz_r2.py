@@ -1,5 +1,5 @@
 """Seeded random cases (-m gpu) for the round-2 paths, every mask against the
-oracle bit for bit: the small-call kernel (single pages up to 2^21 pixels,
+oracle bit for bit: the small-call kernel (single pages up to 2^22 pixels,
 windows up to 64), the packed last strips of page batches (widths just past
 a strip multiple, 2-7 pages), the window-independent Bernsen kernels, and
 the Rais / Feng certified filters on random and document pages."""

@@ -1,5 +1,5 @@
 """GPU parity (-m gpu) of the small-call kernel (csrc/small.cuh): single small
-pages (here up to 2^21 pixels, windows up to 64 x 64) go to one launch of a
+pages (here up to 2^22 pixels, windows up to 64 x 64) go to one launch of a
 shared-memory tile kernel -- exact integer window sums, the certified fp32
 residual and the canonical double threshold inline.  Masks and near-tie
 counts must equal the oracle's bit for bit: odd / even windows, windows
@@ -100,7 +100,7 @@ def test_small_kernel_bands_and_streaming_twin(monkeypatch):
 
 
 def test_small_kernel_megapixel_page(monkeypatch):
-    # the size limit is 2^21 pixels for windows up to 32 x 32 (2^20 beyond): a
+    # the size limit is 2^22 pixels: a
     # ragged 1.43 Mpx page (9 x 69 tiles + partial tiles) against the oracle and
     # the streaming kernels, byte and bit masks
     J = synth.page(1100, 1301, synth.config_seed(2, 3))
@@ -114,8 +114,17 @@ def test_small_kernel_megapixel_page(monkeypatch):
         monkeypatch.delenv("ABIN_SMALL_PX")
         assert np.array_equal(a, ref) and np.array_equal(b, ref), (h, w)
         assert np.array_equal(ab_bits, oracle.pack_bits(ref)), (h, w)
-    # 61 x 61 on the same page is past the 2^20 limit of the wide windows: both routes agree
+    # 61 x 61 (Wolf: the page minimum from the device) on the same page and on its first 800 rows
     ref = oracle.binarize("wolf", J, 61, 61, 0.5, 128.0)
     assert np.array_equal(ab.wolf(x, 61, 61, 0.5, 128.0).cpu().numpy(), ref)
-    K = np.ascontiguousarray(J[:800])   # 1.04 Mpx <= 2^20: the tile kernel at 61 x 61
+    K = np.ascontiguousarray(J[:800])
     assert np.array_equal(ab.wolf(to_dev(K), 61, 61, 0.5, 128.0).cpu().numpy(), oracle.binarize("wolf", K, 61, 61, 0.5, 128.0))
+    # near the 2^22-pixel limit: the tile kernel's masks equal the streaming kernels'
+    # (themselves pinned to the oracle at full size in test_gpu_fullsize.py)
+    B = to_dev(synth.page(2040, 2050, synth.config_seed(2, 4)))
+    for (h, w, packed) in ((15, 15, False), (33, 64, True)):
+        a = ab.niblack(B, h, w, -0.2, packed=packed).cpu().numpy()
+        monkeypatch.setenv("ABIN_SMALL_PX", "0")
+        b = ab.niblack(B, h, w, -0.2, packed=packed).cpu().numpy()
+        monkeypatch.delenv("ABIN_SMALL_PX")
+        assert np.array_equal(a, b), (h, w)
