@@ -403,6 +403,10 @@ def ours_main(args):
             launches_per_step = 0 if P == 0 else (2 if k >= 0.25 else 1)
         else:
             launches_per_step = 0 if P == 0 else (5 if method == "wolf" else 3)
+        if method != "quantile" and not sweep and not flags and P * H * W <= (1 << 22) and max(h, w) <= 64:
+            # single small pages take the one-launch tile kernel (csrc/small.cuh:
+            # decision inline, no fixup launch); Wolf adds the minimum pre-pass
+            launches_per_step = 0 if P == 0 else (4 if method == "wolf" else 1)
         if sweep:
             launches_per_step = 3 * len(SWEEP)
         l2_note = (f"inputs {step_bytes / 1e9:.2f} GB per rank per step > L2: no flush needed" if n_copies == 1 else
