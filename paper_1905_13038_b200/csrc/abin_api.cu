@@ -654,8 +654,12 @@ int run_small(const MomCall& c, const Window& win) {
   p.h = win.h; p.w = win.w; p.l = win.l; p.r = win.r; p.o = win.o; p.u = win.u;
   p.RWp = (kTW + win.w - 1 + 15 + 15) / 16 * 16;
   p.CWp = (kTW + win.w + 3) / 4 * 4 + 1;
-  p.n_rt = (int32_t)((c.H_out + kTH - 1) / kTH);
   p.n_ct = (int32_t)((c.W + kTW - 1) / kTW);
+  // tile height 32 once 16-row tiles would fill the device several times over
+  // (4 resident CTAs per SM): measured in tools/dev/small_big.py
+  const int64_t tiles16 = (c.H_out + 15) / 16 * p.n_ct * c.n_pages;
+  const int TH = tiles16 > env_int("ABIN_SMALL_TH32", 8, 0, 1 << 20) * num_sms() ? 32 : 16;
+  p.n_rt = (int32_t)((c.H_out + TH - 1) / TH);
   const FilterConsts f5 = filter_consts_v5(c.method, c.k, c.R, c.rprm);
   p.fa = f5.fa; p.fb = f5.fb; p.delta1 = f5.delta1;
   p.k = c.k; p.R = c.R;
@@ -671,16 +675,19 @@ int run_small(const MomCall& c, const Window& win) {
     k_narrow_u8<<<(unsigned)((c.n_pages + 255) / 256), 256, 0, c.stream>>>(Lw, l8, c.n_pages);
     p.L_page = l8;
   }
-  const size_t smem = smem_bytes(p.RWp, p.CWp, win.h);
-  static bool attr[3][64] = {};
+  const size_t smem = smem_bytes(p.RWp, p.CWp, win.h, TH);
+  static bool attr[3][2][64] = {};
   int dev = 0;
   CK(cudaGetDevice(&dev));
   const int mi = c.method == M_SAUVOLA ? 0 : (c.method == M_NIBLACK ? 1 : 2);
-  const void* kern = mi == 0 ? (const void*)k_small<M_SAUVOLA>
-                             : (mi == 1 ? (const void*)k_small<M_NIBLACK> : (const void*)k_small<M_WOLF>);
-  if (dev >= 0 && dev < 64 && !attr[mi][dev]) {
+  const int ti = TH == 32 ? 1 : 0;
+  const void* kerns[3][2] = {{(const void*)k_small<M_SAUVOLA, 16>, (const void*)k_small<M_SAUVOLA, 32>},
+                             {(const void*)k_small<M_NIBLACK, 16>, (const void*)k_small<M_NIBLACK, 32>},
+                             {(const void*)k_small<M_WOLF, 16>, (const void*)k_small<M_WOLF, 32>}};
+  const void* kern = kerns[mi][ti];
+  if (dev >= 0 && dev < 64 && !attr[mi][ti][dev]) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr[mi][dev] = true;
+    attr[mi][ti][dev] = true;
   }
   void* args[] = {&p};
   const int64_t n = (int64_t)p.n_rt * p.n_ct * c.n_pages;

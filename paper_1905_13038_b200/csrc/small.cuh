@@ -27,9 +27,8 @@
 namespace abin {
 namespace sm {
 
-constexpr int kTH = 16, kTW = 128, kNT = 256;
-constexpr int kRPW = kTH / (kNT / 32);  // output rows per warp in steps 2b, 3
-static_assert(kRPW * (kNT / 32) == kTH && kTW % 64 == 0, "step 3: a warp takes kRPW rows, a lane pairs of 32-column groups");
+constexpr int kTH = 16, kTW = 128, kNT = 256;  // kTH: the default tile height (the kernel's TH: 16 or 32)
+static_assert(kTH % (kNT / 32) == 0 && kTW % 64 == 0, "step 3: a warp takes kRPW rows, a lane pairs of 32-column groups");
 constexpr int kMaxWin = 64;  // h, w (effective) of the small path
 
 struct SmallParams {
@@ -51,16 +50,20 @@ struct SmallParams {
 };
 
 // region bytes rounded up to 16 (the sums that follow are 32-bit words)
-__host__ __device__ inline size_t region_bytes(int RWp, int h) { return (size_t)(kTH + h - 1) * RWp; }
-__host__ __device__ inline size_t smem_bytes(int RWp, int CWp, int h) {
-  return region_bytes(RWp, h) + (size_t)2 * kTH * CWp * 4;
+__host__ __device__ inline size_t region_bytes(int RWp, int h, int TH) { return (size_t)(TH + h - 1) * RWp; }
+__host__ __device__ inline size_t smem_bytes(int RWp, int CWp, int h, int TH) {
+  return region_bytes(RWp, h, TH) + (size_t)2 * TH * CWp * 4;
 }
 
 #ifndef ABIN_SMALL_MINB
 #define ABIN_SMALL_MINB 4  // resident CTAs per SM the register budget is set for (64 registers; 1: 80 registers, 1024^2 pages 15 % slower)
 #endif
-template <int METHOD>
+// TH: the tile height -- 16 (more tiles: latency of single small pages) or 32
+// (pages of several waves of tiles: the h - 1 re-staged rows and the column
+// sums' start-up are amortised over twice the rows)
+template <int METHOD, int TH>
 __global__ void __launch_bounds__(kNT, ABIN_SMALL_MINB) k_small(const SmallParams p) {
+  constexpr int RPW = TH / (kNT / 32);  // output rows per warp in steps 2b, 3
   extern __shared__ __align__(16) uint8_t smem[];
   const int tid = threadIdx.x;
   uint32_t b = blockIdx.x;  // < 2^31 tiles: 32-bit divisions
@@ -68,11 +71,11 @@ __global__ void __launch_bounds__(kNT, ABIN_SMALL_MINB) k_small(const SmallParam
   b /= (uint32_t)p.n_ct;
   const int rt = (int)(b % (uint32_t)p.n_rt);
   const int page = (int)(b / (uint32_t)p.n_rt);
-  const int64_t i0 = p.row0 + (int64_t)rt * kTH, j0 = (int64_t)ct * kTW;
-  const int RH = kTH + p.h - 1, RW = kTW + p.w - 1, RWp = p.RWp, CWp = p.CWp;
+  const int64_t i0 = p.row0 + (int64_t)rt * TH, j0 = (int64_t)ct * kTW;
+  const int RH = TH + p.h - 1, RW = kTW + p.w - 1, RWp = p.RWp, CWp = p.CWp;
   uint8_t* reg = smem;                                                 // [RH][RWp]
-  uint32_t* Cs = reinterpret_cast<uint32_t*>(smem + region_bytes(RWp, p.h));  // [kTH][CWp]
-  uint32_t* Ds = Cs + kTH * CWp;
+  uint32_t* Cs = reinterpret_cast<uint32_t*>(smem + region_bytes(RWp, p.h, TH));  // [TH][CWp]
+  uint32_t* Ds = Cs + TH * CWp;
   const uint8_t* pg = p.in + (int64_t)page * p.in_page_stride;
   const int64_t y0 = i0 - p.o + 1, x0 = j0 - p.l + 1;                 // region origin (global)
 
@@ -127,7 +130,7 @@ __global__ void __launch_bounds__(kNT, ABIN_SMALL_MINB) k_small(const SmallParam
     }
   }
   __syncthreads();
-  // 2. vertical sums of each region column for the kTH output rows
+  // 2. vertical sums of each region column for the TH output rows
   for (int x = tid; x < RW; x += kNT) {
     uint32_t c = 0, d = 0;
 #pragma unroll 4
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(kNT, ABIN_SMALL_MINB) k_small(const SmallParam
     Cs[x] = c;
     Ds[x] = d;
 #pragma unroll 4
-    for (int t = 1; t < kTH; ++t) {
+    for (int t = 1; t < TH; ++t) {
       const uint32_t vi = reg[(t + p.h - 1) * RWp + dx + x], vo = reg[(t - 1) * RWp + dx + x];
       c += vi - vo;
       d += vi * vi - vo * vo;
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__(kNT, ABIN_SMALL_MINB) k_small(const SmallParam
     }
   }
   __syncthreads();
-  // 2b. each warp turns its kRPW rows of C and D into exclusive prefix sums
+  // 2b. each warp turns its RPW rows of C and D into exclusive prefix sums
   // along the row (RW + 1 entries: P[x] = C[0] + .. + C[x-1], uint32 wraps
   // cancel in differences), so that the window sums of PAPER.md:119-120 are
   // c(j) = P[j + w] - P[j] for any thread-to-column mapping: step 3 reads
@@ -159,8 +162,8 @@ __global__ void __launch_bounds__(kNT, ABIN_SMALL_MINB) k_small(const SmallParam
     const int NP = RW + 1;             // <= 192 = 32 lanes x 6 (RW <= 128 + 64 - 1)
     constexpr int chunk = 6;
 #pragma unroll 1
-    for (int q = 0; q < 2 * kRPW; ++q) {
-      uint32_t* A = ((q & 1) ? Ds : Cs) + (kRPW * wid + (q >> 1)) * CWp;
+    for (int q = 0; q < 2 * RPW; ++q) {
+      uint32_t* A = ((q & 1) ? Ds : Cs) + (RPW * wid + (q >> 1)) * CWp;
       uint32_t v[6], sum = 0;
 #pragma unroll
       for (int k = 0; k < 6; ++k) {
@@ -185,7 +188,7 @@ __global__ void __launch_bounds__(kNT, ABIN_SMALL_MINB) k_small(const SmallParam
     }
   }
   __syncwarp();
-  // 3. a warp = its kRPW rows; a lane = the columns lane, lane + 32, lane + 64,
+  // 3. a warp = its RPW rows; a lane = the columns lane, lane + 32, lane + 64,
   // lane + 96 of the tile: window sums from the prefix rows, then the decision
   const float Lf = METHOD == M_WOLF ? (float)(p.L_fixed >= 0 ? p.L_fixed : (int)p.L_page[page]) : 0.0f;
   v5::f2 fa2, fb2;
@@ -202,10 +205,10 @@ __global__ void __launch_bounds__(kNT, ABIN_SMALL_MINB) k_small(const SmallParam
     ncl[q] = j < Wi ? (uint32_t)(min(j + p.r, Wi - 1) - max(j - p.l, -1)) : 1u;
     rcol[q] = __frcp_rn((float)ncl[q]);
   }
-  uint8_t* orow = p.out + (int64_t)page * p.out_page_stride + (i0 + kRPW * wid - p.row0) * p.out_pitch - p.out_pitch;
+  uint8_t* orow = p.out + (int64_t)page * p.out_page_stride + (i0 + RPW * wid - p.row0) * p.out_pitch - p.out_pitch;
 #pragma unroll 1
-  for (int rr = 0; rr < kRPW; ++rr) {
-    const int t = kRPW * wid + rr;
+  for (int rr = 0; rr < RPW; ++rr) {
+    const int t = RPW * wid + rr;
     const int64_t i = i0 + t;
     if (i >= p.row0 + p.H_out) break;  // warp-uniform
     const uint32_t* Pc = Cs + t * CWp;

@@ -128,3 +128,18 @@ def test_small_kernel_megapixel_page(monkeypatch):
         b = ab.niblack(B, h, w, -0.2, packed=packed).cpu().numpy()
         monkeypatch.delenv("ABIN_SMALL_PX")
         assert np.array_equal(a, b), (h, w)
+
+
+def test_small_kernel_tall_tiles(monkeypatch):
+    # 32-row tiles (taken when 16-row tiles would number more than 8 per SM;
+    # ABIN_SMALL_TH32=0 forces them): ragged page heights around the tile
+    # height, the three rules, byte and bit masks, against the oracle
+    monkeypatch.setenv("ABIN_SMALL_TH32", "0")
+    for (H, W, h, w) in ((33, 130, 5, 7), (95, 257, 32, 32), (64, 128, 64, 64), (1, 300, 9, 3)):
+        I = synth.page(H, W, synth.config_seed(1, H))
+        x = to_dev(I)
+        for method in ("sauvola", "niblack", "wolf"):
+            k, R = PARAMS[method]
+            ref = oracle.binarize(method, I, h, w, k, R)
+            assert np.array_equal(run(method, x, h, w).cpu().numpy(), ref), (method, H, W, h, w)
+            assert np.array_equal(run(method, x, h, w, packed=True).cpu().numpy(), oracle.pack_bits(ref)), (method, H, W)
